@@ -1,0 +1,108 @@
+/*
+ * seghull_b200 -- C ABI of the B200-native Quickhull (drop-in for the hull
+ * entry points of the reference package `seghull`).
+ *
+ * Replaces (reference, /root/reference/pkg/src/seghull/):
+ *   quickhull_2d(points, tol) -> HullResult      quickhull.py:167-279
+ *   quickhull_3d(points, tol) -> HullResult      quickhull.py:282-446
+ *   Tolerance.effective (eps = eps_rel * hypot.reduce(bbox spans))
+ *                                                geometry.py:68-83
+ *   exceptions ContractViolation / EmptyInputError / DegenerateInputError
+ *                                                errors.py:4-15
+ *   AssertionError("round count exceeded ...")   quickhull.py:227-228
+ * The reference has no FFI layer; its boundary is the Python function pair
+ * above.  The Python shim paper_1201_2936_b200/quickhull.py keeps those
+ * names and raises the same exception classes from the status codes below.
+ *
+ * All pointers passed to the hull calls are DEVICE pointers (CUDA), except
+ * `res`.  Coordinates are fp64; `stride` is the element distance between
+ * consecutive points of one coordinate array (1 for structure-of-arrays,
+ * dim for a row-major (n, dim) array).  Indices written to out_idx are
+ * original point indices (int64), in discovery order (first-split extremes,
+ * then per round per segment).  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  One context per device; a context is not thread-safe.
+ */
+#ifndef SEGHULL_B200_H
+#define SEGHULL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define SH_OK 0
+#define SH_CONTRACT 1     /* ContractViolation (bad arguments)              */
+#define SH_EMPTY 2        /* EmptyInputError   (n == 0)                     */
+#define SH_DEGENERATE 3   /* DegenerateInputError (3D coplanar input)       */
+#define SH_ROUND_GUARD 4  /* AssertionError round count exceeded n + 1      */
+#define SH_NOMEM 5        /* device allocation failed                       */
+#define SH_CUDA 10        /* CUDA error, see sh_last_error()                */
+
+/* result flags */
+#define SH_FLAG_COLLINEAR 1 /* "collinear input: ..." warning (2D :208, 3D :338) */
+
+typedef struct sh_ctx sh_ctx;
+
+typedef struct sh_result {
+  int64_t h;          /* vertex indices written to out_idx                   */
+  int64_t iterations; /* Quickhull rounds (HullResult.iterations)            */
+  int64_t candidates; /* 3D: loop candidates before the extreme filter       */
+  int64_t pruned;     /* 3D: candidates removed by the extreme filter        */
+  int64_t facets;     /* 3D: facet triples written (0 if not requested)      */
+  int32_t status;     /* SH_* status                                         */
+  int32_t flags;      /* SH_FLAG_*                                           */
+  double eps;         /* effective absolute tolerance used                   */
+} sh_result;
+
+/* Context management. */
+int sh_create(int device, sh_ctx** out);
+void sh_destroy(sh_ctx* ctx);
+
+/* 2D hull.  eps_abs: NaN -> eps = eps_rel * glibc_hypot(bbox spans)
+ * (Tolerance.effective); otherwise eps_abs is used as the absolute eps
+ * (sharded runs share the global eps).  out_idx: capacity n.
+ * Synchronous w.r.t. `stream` (returns after the result is known). */
+int sh_hull2d(sh_ctx* ctx, const double* x, const double* y, int64_t stride, int64_t n,
+              double eps_rel, double eps_abs, int64_t* out_idx, sh_result* res, void* stream);
+
+/* 3D hull: vertex indices of the extreme points (reference result after
+ * _extreme_vertex_mask, quickhull.py:136-164).  out_facets (optional, may
+ * be NULL): int32 triples (i, j, k) of original indices, counter-clockwise
+ * seen from outside, capacity facet_cap triples. */
+int sh_hull3d(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride,
+              int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* out_facets,
+              int64_t facet_cap, sh_result* res, void* stream);
+
+/* Asynchronous variants: enqueue the whole hull (one CUDA-graph launch, no
+ * host synchronisation inside the round loop) and return immediately;
+ * sh_fetch() waits for the stream and fills `res`. */
+int sh_hull2d_async(sh_ctx* ctx, const double* x, const double* y, int64_t stride, int64_t n,
+                    double eps_rel, double eps_abs, int64_t* out_idx, void* stream);
+int sh_hull3d_async(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride,
+                    int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* out_facets,
+                    int64_t facet_cap, void* stream);
+int sh_fetch(sh_ctx* ctx, sh_result* res, void* stream);
+
+/* Per-round counters of the last hull on this context (live points
+ * entering, survivors, segments, near-coplanar segments dropped); returns
+ * the number of rounds written (<= cap). */
+int64_t sh_trace(sh_ctx* ctx, int64_t* live, int64_t* kept, int64_t* nseg, int64_t* flat,
+                 int64_t cap);
+
+/* Reserve workspace for `dim`-D hulls of up to n points (optional). */
+int sh_reserve(sh_ctx* ctx, int dim, int64_t n);
+
+/* Host-side self test of the glibc-hypot port used for eps and 2D edge
+ * lengths (no GPU needed). */
+void sh_hypot_host(const double* x, const double* y, double* out, int64_t n);
+
+const char* sh_last_error(void);
+const char* sh_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEGHULL_B200_H */

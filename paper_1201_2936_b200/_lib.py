@@ -1,0 +1,104 @@
+"""ctypes binding of the in-tree C-ABI library ``libseghull_b200.so``
+(declarations: include/seghull_b200.h).
+
+There is no CPU fallback: if the library (or a CUDA device) is missing,
+every hull call raises.
+"""
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libseghull_b200.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+SH_OK, SH_CONTRACT, SH_EMPTY, SH_DEGENERATE, SH_ROUND_GUARD, SH_NOMEM, SH_CUDA = 0, 1, 2, 3, 4, 5, 10
+SH_FLAG_COLLINEAR = 1
+
+EXPORTED = ("sh_create", "sh_destroy", "sh_hull2d", "sh_hull3d", "sh_hull2d_async",
+            "sh_hull3d_async", "sh_fetch", "sh_trace", "sh_reserve", "sh_hypot_host",
+            "sh_last_error", "sh_version")
+
+
+class ShResult(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_int64), ("iterations", ctypes.c_int64),
+                ("candidates", ctypes.c_int64), ("pruned", ctypes.c_int64),
+                ("facets", ctypes.c_int64), ("status", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("eps", ctypes.c_double)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def build(force=False):
+    """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles
+    without a GPU)."""
+    cmd = ["make", "-s", "-C", CSRC]
+    if force:
+        subprocess.run(["make", "-s", "-C", CSRC, "clean"], check=True)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `make -C {CSRC}` "
+                    "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+            L.sh_create.argtypes = [ctypes.c_int, ctypes.POINTER(P)]
+            L.sh_create.restype = ctypes.c_int
+            L.sh_destroy.argtypes = [P]
+            L.sh_destroy.restype = None
+            L.sh_hull2d.argtypes = [P, P, P, I64, I64, D, D, P, ctypes.POINTER(ShResult), P]
+            L.sh_hull2d.restype = ctypes.c_int
+            L.sh_hull3d.argtypes = [P, P, P, P, I64, I64, D, D, P, P, I64,
+                                    ctypes.POINTER(ShResult), P]
+            L.sh_hull3d.restype = ctypes.c_int
+            L.sh_hull2d_async.argtypes = [P, P, P, I64, I64, D, D, P, P]
+            L.sh_hull2d_async.restype = ctypes.c_int
+            L.sh_hull3d_async.argtypes = [P, P, P, P, I64, I64, D, D, P, P, I64, P]
+            L.sh_hull3d_async.restype = ctypes.c_int
+            L.sh_fetch.argtypes = [P, ctypes.POINTER(ShResult), P]
+            L.sh_fetch.restype = ctypes.c_int
+            L.sh_trace.argtypes = [P, P, P, P, P, I64]
+            L.sh_trace.restype = I64
+            L.sh_reserve.argtypes = [P, ctypes.c_int, I64]
+            L.sh_reserve.restype = ctypes.c_int
+            L.sh_hypot_host.argtypes = [P, P, P, I64]
+            L.sh_hypot_host.restype = None
+            L.sh_last_error.argtypes = []
+            L.sh_last_error.restype = ctypes.c_char_p
+            L.sh_version.argtypes = []
+            L.sh_version.restype = ctypes.c_char_p
+            _lib = L
+        return _lib
+
+
+def last_error():
+    return lib().sh_last_error().decode()
+
+
+_ctx = {}
+
+
+def context(device: int):
+    """One C-ABI context per device (workspace + captured CUDA graphs)."""
+    with _lock:
+        c = _ctx.get(device)
+    if c is None:
+        h = ctypes.c_void_p()
+        rc = lib().sh_create(device, ctypes.byref(h))
+        if rc != SH_OK:
+            raise RuntimeError(f"sh_create failed ({rc}): {last_error()}")
+        with _lock:
+            _ctx[device] = h
+        c = h
+    return c

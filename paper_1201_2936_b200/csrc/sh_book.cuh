@@ -1,0 +1,284 @@
+// K3: per-segment bookkeeping between rounds.
+//
+// Input: the child results written by the round kernel into `slots`
+// (stream-order child id e = s*nseg_parent + parent: farthest key, lowest
+// index, count).  One persistent launch, one thread per child:
+//   * occupied children (count > 0) get dense ids by a decoupled look-back
+//     scan over (occupied, count, emitted) -- the dense order is the stream
+//     order, which is exactly the order the round kernel wrote the
+//     survivors in, so the scanned counts are the segments' start positions;
+//   * child tables are built once per segment (2D: the child edge and the
+//     three glibc-exact hypot thresholds, quickhull.py:268-277 and
+//     geometry.py:150-156; 3D: face normal, |n|, flat-segment test
+//     quickhull.py:384-389, side faces of the next tetrahedron);
+//   * the farthest point of every non-flat child is emitted as a hull vertex
+//     (quickhull.py:236-240 / :390-391);
+//   * the finalising tile writes the next round's launch parameters and the
+//     CUDA-graph WHILE condition (live points remain), so the host never
+//     synchronises inside the loop (quickhull.py:225 / :367 become a device
+//     flag).
+#pragma once
+
+#include "sh_common.cuh"
+
+namespace sh {
+
+struct BookShared {
+  uint32_t tile;
+  uint32_t wsum[ITEMS3 * WARPS * 3];
+  Sum3 agg, prefix;
+  Sum3 window[32];
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
+  constexpr int K = DIM;
+  DevState* st = ws.st;
+  __shared__ BookShared sb;
+  const BookParams bp = st->bp;
+  if (!bp.active) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nsp = bp.nseg_parent;
+  const uint32_t E = K * nsp;
+  const uint32_t num_tiles = (E + TILE3 - 1) / TILE3;
+  const uint32_t tag = bp.tag;
+  const double eps = st->eps;
+  const uint32_t segcap = st->segcap;
+  const int64_t stride = st->stride;
+  const uint32_t in_b = bp.cur, out_b = bp.cur ^ 1u;
+  const Seg2* par2 = reinterpret_cast<const Seg2*>(ws.seg[in_b]);
+  const Seg3* par3 = reinterpret_cast<const Seg3*>(ws.seg[in_b]);
+  Seg2* ch2 = reinterpret_cast<Seg2*>(ws.seg[out_b]);
+  Seg3* ch3 = reinterpret_cast<Seg3*>(ws.seg[out_b]);
+  uint32_t* segstart = ws.segstart[out_b];
+  uint32_t* tile_seg = ws.tile_seg[out_b];
+
+  while (true) {
+    if (tid == 0) sb.tile = atomicAdd(&st->ctr_book, 1u);
+    __syncthreads();
+    const uint32_t tile = sb.tile;
+    if (tile >= num_tiles) break;
+    const uint32_t base = tile * TILE3;
+    const bool last_tile = tile == num_tiles - 1;
+
+    RunVal v[ITEMS3];
+    uint32_t cval[ITEMS3][3];
+    // 3D child face (needed before the scan for the flat test)
+    double fa[ITEMS3][3], fb[ITEMS3][3], fc[ITEMS3][3], fn[ITEMS3][3], fnl[ITEMS3];
+#pragma unroll
+    for (int j = 0; j < ITEMS3; j++) {
+      uint32_t e = base + j * BLOCK + tid;
+      v[j].hi = 0;
+      v[j].idx = 0;
+      v[j].cnt = 0;
+      if (e < E) {
+        v[j] = ld_cg(&ws.slots[e]);
+        if (v[j].cnt) {
+          RunVal z;
+          z.hi = 0;
+          z.idx = 0;
+          z.cnt = 0;
+          st_cg(&ws.slots[e], z);  // slots are all-zero between uses
+        }
+      }
+      bool occ = v[j].cnt > 0;
+      bool emit = occ;
+      if (DIM == 3 && occ) {
+        uint32_t s = e / nsp, p = e - s * nsp;
+        const double *A, *B, *C;
+        if (bp.root) {  // quickhull.py:359-364
+          A = st->pa;
+          B = (s == 0) ? st->pb : st->pc;
+          C = (s == 0) ? st->pc : st->pb;
+        } else {        // children (a,b,f), (b,c,f), (c,a,f), quickhull.py:419-423
+          const Seg3& P = par3[p];
+          A = (s == 0) ? P.a : (s == 1 ? P.b : P.c);
+          B = (s == 0) ? P.b : (s == 1 ? P.c : P.a);
+          C = P.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          fa[j][k] = A[k];
+          fb[j][k] = B[k];
+          fc[j][k] = C[k];
+        }
+        face_normal(fa[j], fb[j], fc[j], fn[j]);
+        fnl[j] = norm3(fn[j]);
+        // flat_seg = seg_max <= eps * nlen (quickhull.py:385)
+        emit = !(from_ordered_bits(v[j].hi) <= mul(eps, fnl[j]));
+      }
+      cval[j][0] = occ ? 1u : 0u;
+      cval[j][1] = v[j].cnt;
+      cval[j][2] = emit ? 1u : 0u;
+    }
+    // ---- block exclusive scan (striped order) of the three counters
+    uint32_t ex[ITEMS3][3];
+#pragma unroll
+    for (int j = 0; j < ITEMS3; j++) {
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        uint32_t x = cval[j][q];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          uint32_t o = __shfl_up_sync(0xFFFFFFFFu, x, off);
+          if (lane >= off) x += o;
+        }
+        ex[j][q] = x - cval[j][q];
+        if (lane == 31) sb.wsum[(j * WARPS + warp) * 3 + q] = x;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      Sum3 a;
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        uint32_t w = sb.wsum[lane * 3 + q];
+        uint32_t x = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          uint32_t o = __shfl_up_sync(0xFFFFFFFFu, x, off);
+          if (lane >= off) x += o;
+        }
+        sb.wsum[lane * 3 + q] = x - w;
+        a.v[q] = __shfl_sync(0xFFFFFFFFu, x, 31);
+      }
+      a.v[3] = 0;
+      Sum3 pre = s3_identity();
+      if (tile == 0) {
+        lookback_publish_incl<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_incl_book, tile,
+                                                                tag, &a);
+      } else {
+        lookback_publish_agg<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_agg_book, tile,
+                                                               tag, &a);
+        lookback_wait<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_agg_book,
+                                                        ws.lb_incl_book, tile, tag, sb.window, &pre);
+        Sum3 inc = s3_combine(pre, a);
+        lookback_publish_incl<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_incl_book, tile,
+                                                                tag, &inc);
+      }
+      if (lane == 0) {
+        sb.prefix = pre;
+        sb.agg = a;
+      }
+    }
+    __syncthreads();
+
+    // ---- build child tables, emit vertices
+#pragma unroll
+    for (int j = 0; j < ITEMS3; j++) {
+      if (!cval[j][0]) continue;
+      uint32_t e = base + j * BLOCK + tid;
+      uint32_t s = e / nsp, p = e - s * nsp;
+      const uint32_t* wo = &sb.wsum[(j * WARPS + warp) * 3];
+      uint32_t c = sb.prefix.v[0] + wo[0] + ex[j][0];
+      uint32_t start = sb.prefix.v[1] + wo[1] + ex[j][1];
+      uint32_t vpos = sb.prefix.v[2] + wo[2] + ex[j][2];
+      uint32_t far = v[j].idx;
+      if (cval[j][2]) ws.vout[bp.h + vpos] = far;
+      if (c >= segcap) continue;  // overflow: reported by the finalising tile
+      segstart[c] = start;
+      {  // first segment of every next-round tile that starts inside [start, start+cnt)
+        uint32_t t0 = (start + TILE - 1) / TILE, t1 = (start + v[j].cnt - 1) / TILE;
+        for (uint32_t t = t0; t <= t1; t++) tile_seg[t] = c;
+      }
+      double F[3];
+      F[0] = ld_coord(st->px, stride, far);
+      F[1] = ld_coord(st->py, stride, far);
+      F[2] = (DIM == 3) ? ld_coord(st->pz, stride, far) : 0.0;
+      if (DIM == 2) {
+        double Ax, Ay, Bx, By;
+        if (bp.root) {  // quickhull.py:217-222
+          Ax = (s == 0) ? st->pa[0] : st->pb[0];
+          Ay = (s == 0) ? st->pa[1] : st->pb[1];
+          Bx = (s == 0) ? st->pb[0] : st->pa[0];
+          By = (s == 0) ? st->pb[1] : st->pa[1];
+        } else {        // (a, far) / (far, b), quickhull.py:272-277
+          const Seg2& P = par2[p];
+          Ax = (s == 0) ? P.ax : P.fx;
+          Ay = (s == 0) ? P.ay : P.fy;
+          Bx = (s == 0) ? P.fx : P.bx;
+          By = (s == 0) ? P.fy : P.by;
+        }
+        Seg2 g;
+        g.ax = Ax; g.ay = Ay; g.bx = Bx; g.by = By; g.fx = F[0]; g.fy = F[1];
+        // point_in_triangle(a, b, far): -eps * edge_length(.,.) per edge
+        g.nt_ab = mul(-eps, edge_length(Ax, Ay, Bx, By));
+        g.nt_bf = mul(-eps, edge_length(Bx, By, F[0], F[1]));
+        g.nt_fa = mul(-eps, edge_length(F[0], F[1], Ax, Ay));
+        g.fidx = far;
+        g.pad = 0;
+        ch2[c] = g;
+      } else {
+        Seg3 g;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          g.a[k] = fa[j][k];
+          g.b[k] = fb[j][k];
+          g.c[k] = fc[j][k];
+          g.n[k] = fn[j][k];
+          g.f[k] = F[k];
+        }
+        g.nt_base = mul(-eps, fnl[j]);  // point_in_tetrahedron base test (geometry.py:172)
+        g.fidx = far;
+        g.flat = cval[j][2] ? 0u : 1u;
+        // side faces (a,b,f), (b,c,f), (c,a,f), geometry.py:166-175
+        face_normal(g.a, g.b, F, g.N[0]);
+        face_normal(g.b, g.c, F, g.N[1]);
+        face_normal(g.c, g.a, F, g.N[2]);
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          g.nrm[q] = norm3(g.N[q]);
+          g.thr[q] = mul(eps, g.nrm[q]);
+        }
+        ch3[c] = g;
+      }
+    }
+
+    // ---- finalise the launch: next round's parameters + loop condition
+    if (last_tile && tid == 0) {
+      Sum3 T = s3_combine(sb.prefix, sb.agg);
+      uint32_t nseg_next = T.v[0], n_next = T.v[1], emitted = T.v[2];
+      uint32_t status = st->status;
+      uint32_t round_next = bp.round + 1;  // the round the children belong to
+      if (bp.root && DIM == 3) {
+        // quickhull.py:349-351 -- every point within eps of the first plane
+        double dmax = __longlong_as_double((long long)st->dmax_bits);
+        if (dmax <= mul(eps, st->nlen)) status = ST_DEGENERATE;
+      }
+      if (bp.root && DIM == 2 && n_next == 0 && st->n > 2) st->flags |= FL_COLLINEAR;  // :206-209
+      if (nseg_next > segcap) {
+        status = ST_SEG_OVERFLOW;
+        st->seg_needed = nseg_next;
+      } else {
+        segstart[nseg_next] = n_next;
+      }
+      if (DIM == 3 && round_next - 1 < MAX_TRACE) st->tr_flat[round_next - 1] = nseg_next - emitted;
+      uint32_t h_next = bp.h + emitted;
+      bool cont = (n_next > 0) && status == ST_OK;
+      if (cont && (uint64_t)round_next > (uint64_t)st->n + 1) {  // quickhull.py:227-228
+        status = ST_ROUND_GUARD;
+        cont = false;
+      }
+      RoundParams rp;
+      rp.active = cont ? 1u : 0u;
+      rp.n_live = n_next;
+      rp.nseg = nseg_next;
+      for (int s = 0; s < 4; s++) rp.cnt_in[s] = bp.cnt_out[s];
+      rp.cur = out_b;
+      rp.h = h_next;
+      rp.round = bp.round;
+      rp.tag = tag + 1;
+      st->rp = rp;
+      st->status = status;
+      st->h_final = h_next;
+      st->rounds_final = bp.round;
+      st->seq = tag + 1;
+      st->ctr_round = 0;
+      st->bp.active = 0;
+      if (ws.use_cond) cudaGraphSetConditional(ws.cond, cont ? 1u : 0u);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace sh

@@ -1,0 +1,382 @@
+// Shared device-side types for the B200 Quickhull path.
+//
+// Data layout in HBM:
+//   * live points of a round are structure-of-arrays records
+//     (x, y[, z] fp64 + uint32 original index) split into K = dim "streams";
+//     stream s holds the survivors whose child state is s, in input order,
+//     so every child segment (s, parent) is one contiguous run.  The next
+//     round reads the K streams back to back ("logical" positions).
+//   * per-segment tables (Seg2 / Seg3) hold everything a point needs to be
+//     classified against its segment's simplex, built once per segment by
+//     the bookkeeping kernel (K3), never per element (the reference gathers
+//     the per-segment edge/face data to every element, quickhull.py:231-233,
+//     :373-375).
+//   * child results (farthest point key + count) are written once per child
+//     into `slots` indexed by the child's stream-order id e = s*nseg + parent.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sh_numerics.cuh"
+
+namespace sh {
+
+constexpr int BLOCK = 256;
+constexpr int WARPS = BLOCK / 32;
+constexpr int ITEMS = 8;             // points per thread per tile (round kernel)
+constexpr int TILE = BLOCK * ITEMS;  // 2048 points per tile
+constexpr int ITEMS3 = 4;            // children per thread per tile (bookkeeping kernel)
+constexpr int TILE3 = BLOCK * ITEMS3;
+constexpr int MAX_TRACE = 4096;      // per-round counters kept on device
+
+// status codes (C ABI, include/seghull_b200.h)
+constexpr uint32_t ST_OK = 0;
+constexpr uint32_t ST_EMPTY = 2;
+constexpr uint32_t ST_DEGENERATE = 3;
+constexpr uint32_t ST_ROUND_GUARD = 4;
+constexpr uint32_t ST_SEG_OVERFLOW = 6;
+
+constexpr uint32_t FL_COLLINEAR = 1;
+
+// Farthest-point aggregate of a run of points (one child segment).
+// Larger `hi` (order-preserving bits of the distance) wins, ties go to the
+// lowest original index (quickhull.py:93-100: first max in a segment whose
+// elements are in ascending original-index order).  cnt sums.
+struct __align__(16) RunVal {
+  uint64_t hi;
+  uint32_t idx;
+  uint32_t cnt;
+};
+
+SH_HD RunVal rv_merge(RunVal a, RunVal b) {
+  RunVal r;
+  bool take_b = (b.hi > a.hi) || (b.hi == a.hi && b.idx < a.idx);
+  r.hi = take_b ? b.hi : a.hi;
+  r.idx = take_b ? b.idx : a.idx;
+  r.cnt = a.cnt + b.cnt;
+  return r;
+}
+
+// Look-back payload of one stream over a range of tiles: a reduce-by-key
+// state (segmented reduction over the sorted child keys of that stream).
+struct __align__(16) StreamAgg {
+  uint32_t n;       // elements
+  uint32_t fkey;    // key of the first element
+  uint32_t lkey;    // key of the last element
+  uint32_t single;  // 1 if every element has the same key
+  RunVal lval;      // aggregate of the last run restricted to the range
+};
+
+SH_HD StreamAgg sa_identity() {
+  StreamAgg a;
+  a.n = 0; a.fkey = 0; a.lkey = 0; a.single = 1;
+  a.lval.hi = 0; a.lval.idx = 0xFFFFFFFFu; a.lval.cnt = 0;
+  return a;
+}
+
+// a covers older tiles, b newer ones.
+SH_HD StreamAgg sa_combine(StreamAgg a, StreamAgg b) {
+  if (b.n == 0) return a;
+  if (a.n == 0) return b;
+  StreamAgg r;
+  bool cont = a.lkey == b.fkey;
+  r.n = a.n + b.n;
+  r.fkey = a.fkey;
+  r.lkey = b.lkey;
+  r.single = (a.single && b.single && cont) ? 1u : 0u;
+  r.lval = (b.single && cont) ? rv_merge(a.lval, b.lval) : b.lval;
+  return r;
+}
+
+struct __align__(16) Sum3 {
+  uint32_t v[4];
+};
+
+SH_HD Sum3 s3_identity() { Sum3 s; s.v[0] = s.v[1] = s.v[2] = s.v[3] = 0; return s; }
+SH_HD Sum3 s3_combine(Sum3 a, Sum3 b) {
+  Sum3 r;
+  for (int i = 0; i < 4; i++) r.v[i] = a.v[i] + b.v[i];
+  return r;
+}
+
+// 2D segment: directed split edge a->b (points lie left of it), its
+// farthest point f and the three pre-scaled triangle thresholds
+// (-eps)*|edge| of point_in_triangle (geometry.py:150-156).
+struct __align__(16) Seg2 {
+  double ax, ay, bx, by, fx, fy;
+  double nt_ab, nt_bf, nt_fa;
+  uint32_t fidx, pad;
+};
+
+// 3D segment: face (a, b, c) with outward normal n = (b-a)x(c-a), far point
+// f, and the three side faces (a,b,f), (b,c,f), (c,a,f) of the tetrahedron
+// (geometry.py:163-175) with their normals, norms and eps thresholds.
+struct __align__(16) Seg3 {
+  double a[3], b[3], c[3];
+  double n[3];
+  double nt_base;  // (-eps) * |n|
+  double f[3];
+  double N[3][3];
+  double nrm[3];   // |N_j|
+  double thr[3];   // eps * |N_j|
+  uint32_t fidx, flat;
+};
+
+// Per-launch parameter blocks.  Each kernel reads only its own block and
+// writes the block of the kernel that follows it, so a finalising tile
+// never changes a value that another tile of the same launch still reads.
+struct RoundParams {      // read by the round kernel (K2)
+  uint32_t active;
+  uint32_t n_live;        // points entering the round (logical positions)
+  uint32_t nseg;          // segments of the round
+  uint32_t cnt_in[4];     // per-stream sizes of the live array
+  uint32_t cur;           // ping-pong index of live records / tables
+  uint32_t h;             // vertices emitted so far
+  uint32_t round;         // rounds completed before this one
+  uint32_t tag;           // look-back tag of this launch
+};
+
+struct BookParams {       // read by the bookkeeping kernel (K3)
+  uint32_t active;
+  uint32_t root;          // 1: children of the first split
+  uint32_t nseg_parent;
+  uint32_t cnt_out[4];    // per-stream survivor counts written by K2
+  uint32_t n_out;
+  uint32_t cur;
+  uint32_t h;
+  uint32_t round;         // rounds completed (children belong to round+1)
+  uint32_t tag;
+};
+
+struct DevState {
+  // ---- call parameters (host -> device before every launch) ----
+  const double* px;
+  const double* py;
+  const double* pz;
+  int64_t stride;         // element stride of the coordinate arrays
+  uint32_t n;
+  uint32_t dim;
+  double eps_rel;
+  double eps_abs;
+  uint32_t use_eps_abs;
+  uint32_t segcap;        // capacity of segment tables
+  int64_t* out_idx;       // user output (device), capacity n
+  // ---- first split (K0/K0b) ----
+  double eps;
+  uint32_t imin, imax, ifar;
+  uint32_t first_active;
+  double pa[3], pb[3], pc[3];
+  double nrm[3];
+  double nlen;
+  double thr_line;        // 2D: eps*|pmax-pmin|; 3D: (-eps)*nlen
+  uint64_t dmax_bits;     // 3D coplanarity check: max |d| over the first split
+  // ---- loop ----
+  RoundParams rp;
+  BookParams bp;
+  uint32_t status;
+  uint32_t flags;
+  uint32_t h_final;
+  uint32_t rounds_final;
+  uint32_t seg_needed;    // largest segment count requested (overflow retry)
+  uint32_t seq;           // look-back tag, bumped by every finalising tile
+  uint32_t ctr_round;     // dynamic tile counters
+  uint32_t ctr_book;
+  uint32_t ctr_red;       // last-block counter for reductions
+  uint32_t pad0;
+  // ---- traces (per round r, index r-1) ----
+  uint32_t tr_live[MAX_TRACE];
+  uint32_t tr_kept[MAX_TRACE];
+  uint32_t tr_nseg[MAX_TRACE];
+  uint32_t tr_flat[MAX_TRACE];
+};
+
+// Device buffers of one context (all allocated once, sized for n / segcap).
+struct Workspace {
+  DevState* st;
+  // live records, ping-pong, K regions of capacity rcap each
+  double* rx[2];
+  double* ry[2];
+  double* rz[2];
+  uint32_t* ri[2];
+  uint64_t rcap;
+  // segment tables (ping-pong)
+  void* seg[2];
+  uint32_t* segstart[2];
+  uint32_t* tile_seg[2];
+  // child results, stream-order ids, zero between uses
+  RunVal* slots;
+  // decoupled look-back state
+  uint64_t* lb_flag_round;
+  StreamAgg* lb_agg_round;   // [tiles][4]
+  StreamAgg* lb_incl_round;
+  uint64_t* lb_flag_book;
+  Sum3* lb_agg_book;
+  Sum3* lb_incl_book;
+  // vertex output (uint32 original indices)
+  uint32_t* vout;
+  // reduction partials
+  double* red;               // per block partial records
+  uint32_t red_blocks;
+  uint32_t round_grid;
+  uint32_t book_grid;
+  uint32_t max_tiles;
+  cudaGraphConditionalHandle cond;
+  uint32_t use_cond;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+  return *(const volatile uint64_t*)p;
+}
+__device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
+  *(volatile uint64_t*)p = v;
+}
+
+template <class T>
+__device__ __forceinline__ T ld_cg(const T* p) {
+  static_assert(sizeof(T) % 16 == 0, "16B payloads");
+  T r;
+  const uint4* s = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 16); i++) d[i] = __ldcg(s + i);
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ void st_cg(T* p, const T& v) {
+  static_assert(sizeof(T) % 16 == 0, "16B payloads");
+  uint4* d = reinterpret_cast<uint4*>(p);
+  const uint4* s = reinterpret_cast<const uint4*>(&v);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 16); i++) __stcg(d + i, s[i]);
+}
+
+__device__ __forceinline__ double ld_coord(const double* p, int64_t stride, uint32_t i) {
+  return __ldg(p + (int64_t)i * stride);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <class T>
+__device__ __forceinline__ T shfl_up_t(T v, int off) {
+  static_assert(sizeof(T) % 4 == 0, "");
+  T r;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) d[i] = __shfl_up_sync(0xFFFFFFFFu, s[i], off);
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ T shfl_t(T v, int src) {
+  static_assert(sizeof(T) % 4 == 0, "");
+  T r;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) d[i] = __shfl_sync(0xFFFFFFFFu, s[i], src);
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ T shfl_down_t(T v, int off) {
+  static_assert(sizeof(T) % 4 == 0, "");
+  T r;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) d[i] = __shfl_down_sync(0xFFFFFFFFu, s[i], off);
+  return r;
+}
+
+// Decoupled look-back (single pass chained scan) over tiles with an
+// NP-wide payload per tile.  Status word: (tag << 2) | flag, flag 1 =
+// aggregate published, 2 = inclusive prefix published.  Payloads are
+// written before the status word (fence in between) and read with .cg
+// loads after it.  Executed by one full warp; returns the exclusive prefix
+// (per payload) in lane 0's `prefix`.
+template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
+__device__ void lookback_publish_agg(uint64_t* flags, P* agg, uint32_t tile, uint32_t tag,
+                                     const P* mine) {
+  int lane = threadIdx.x & 31;
+  if (lane < NP) st_cg(&agg[(size_t)tile * NP + lane], mine[lane]);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) st_volatile_u64(&flags[tile], ((uint64_t)tag << 2) | 1ull);
+}
+
+template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
+__device__ void lookback_publish_incl(uint64_t* flags, P* incl, uint32_t tile, uint32_t tag,
+                                      const P* mine) {
+  int lane = threadIdx.x & 31;
+  if (lane < NP) st_cg(&incl[(size_t)tile * NP + lane], mine[lane]);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) st_volatile_u64(&flags[tile], ((uint64_t)tag << 2) | 2ull);
+}
+
+// window: shared scratch of 32*NP payloads.  On return prefix[0..NP) (all
+// lanes) holds the exclusive prefix of `tile`.
+template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
+__device__ void lookback_wait(const uint64_t* flags, const P* agg, const P* incl, uint32_t tile,
+                              uint32_t tag, P* window, P* prefix) {
+  int lane = threadIdx.x & 31;
+  P acc[NP];
+#pragma unroll
+  for (int i = 0; i < NP; i++) acc[i] = IDENT();
+  int64_t pos = (int64_t)tile - 1;
+  while (pos >= 0) {
+    int64_t t = pos - lane;
+    bool valid = t >= 0;
+    uint32_t fl = 0;
+    if (valid) {
+      uint64_t w;
+      do {
+        w = ld_volatile_u64(&flags[t]);
+      } while ((w >> 2) != (uint64_t)tag || (w & 3ull) == 0);
+      fl = (uint32_t)(w & 3ull);
+    }
+    __syncwarp();
+    uint32_t incl_mask = __ballot_sync(0xFFFFFFFFu, valid && fl == 2);
+    uint32_t valid_mask = __ballot_sync(0xFFFFFFFFu, valid);
+    int stop = incl_mask ? (__ffs(incl_mask) - 1) : (31 - __clz(valid_mask));
+    __threadfence();
+    if (lane <= stop) {
+      const P* src = (fl == 2) ? incl : agg;
+#pragma unroll
+      for (int i = 0; i < NP; i++) window[lane * NP + i] = ld_cg(&src[(size_t)t * NP + i]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      P w[NP];
+#pragma unroll
+      for (int i = 0; i < NP; i++) w[i] = IDENT();
+      for (int l = stop; l >= 0; l--) {
+#pragma unroll
+        for (int i = 0; i < NP; i++) w[i] = COMBINE(w[i], window[l * NP + i]);
+      }
+#pragma unroll
+      for (int i = 0; i < NP; i++) acc[i] = COMBINE(w[i], acc[i]);
+    }
+    __syncwarp();
+    if (incl_mask) break;
+    pos -= 32;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NP; i++) window[i] = acc[i];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < NP; i++) prefix[i] = window[i];
+  __syncwarp();
+}
+
+}  // namespace sh

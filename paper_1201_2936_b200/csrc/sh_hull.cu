@@ -1,0 +1,468 @@
+// Host side of the B200 Quickhull: context, workspace, CUDA-graph driver,
+// C ABI (include/seghull_b200.h).
+//
+// One hull call = one CUDA-graph launch:
+//   k_init -> K0 k_first_reduce -> [3D: K0b k_line_far] -> K1 k_round<FIRST>
+//   -> K3 k_book (root) -> WHILE(live points) { K2 k_round ; K3 k_book }
+//   -> [3D: K4 extreme filter] -> k_output
+// The WHILE condition is written by the finalising tile of k_book
+// (cudaGraphSetConditional), so the round loop never returns to the host
+// (the paper's per-iteration "new input size" readback, PAPER.md:292 /
+// quickhull.py:225, is gone).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/seghull_b200.h"
+#include "sh_book.cuh"
+#include "sh_filter3.cuh"
+#include "sh_kernels.cuh"
+#include "sh_round.cuh"
+
+using namespace sh;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+}  // namespace
+
+struct sh_ctx {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t build_stream = nullptr;
+  cudaStream_t body_stream = nullptr;
+  // workspace
+  int dim = 0;           // dim the workspace was sized for (2 or 3), 0 = none
+  uint64_t cap_n = 0;    // points
+  uint32_t segcap = 0;   // segments
+  Workspace ws{};
+  FilterWs fws{};
+  size_t red_bytes = 0;
+  DevState* st_host = nullptr;  // pinned mirror
+  Graph g[4];
+  int round_occ = 0, book_occ = 0;
+  uint32_t last_n = 0;
+};
+
+#define CK(x)                                                                     \
+  do {                                                                            \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess) {                                                      \
+      g_last_error = std::string(#x) + ": " + cudaGetErrorString(e_);             \
+      return SH_CUDA;                                                             \
+    }                                                                             \
+  } while (0)
+
+static int set_err(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, count * sizeof(T) + 64);
+}
+
+static void free_ws(sh_ctx* c) {
+  Workspace& w = c->ws;
+  for (int b = 0; b < 2; b++) {
+    cudaFree(w.rx[b]);
+    cudaFree(w.ry[b]);
+    cudaFree(w.rz[b]);
+    cudaFree(w.ri[b]);
+    cudaFree(w.seg[b]);
+    cudaFree(w.segstart[b]);
+    cudaFree(w.tile_seg[b]);
+  }
+  cudaFree(w.slots);
+  cudaFree(w.lb_flag_round);
+  cudaFree(w.lb_agg_round);
+  cudaFree(w.lb_incl_round);
+  cudaFree(w.lb_flag_book);
+  cudaFree(w.lb_agg_book);
+  cudaFree(w.lb_incl_book);
+  cudaFree(w.vout);
+  cudaFree(w.red);
+  cudaFree(w.st);
+  filter_free(c->fws);
+  DevState* keep = nullptr;
+  (void)keep;
+  w = Workspace{};
+  c->fws = FilterWs{};
+  for (auto& g : c->g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g = Graph{};
+  }
+  c->dim = 0;
+  c->cap_n = 0;
+  c->segcap = 0;
+}
+
+static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap) {
+  free_ws(c);
+  Workspace& w = c->ws;
+  const int K = dim;
+  uint64_t rcap = n + 16;
+  w.rcap = rcap;
+  uint64_t max_tiles = (n + TILE - 1) / TILE + 4;
+  uint64_t book_tiles = ((uint64_t)K * segcap + TILE3 - 1) / TILE3 + 4;
+  size_t seg_bytes = (dim == 2) ? sizeof(Seg2) : sizeof(Seg3);
+  bool ok = true;
+  for (int b = 0; b < 2; b++) {
+    ok &= dalloc(&w.rx[b], K * rcap) == cudaSuccess;
+    ok &= dalloc(&w.ry[b], K * rcap) == cudaSuccess;
+    if (dim == 3) ok &= dalloc(&w.rz[b], K * rcap) == cudaSuccess;
+    ok &= dalloc(&w.ri[b], K * rcap) == cudaSuccess;
+    ok &= cudaMalloc(&w.seg[b], (size_t)segcap * seg_bytes + 256) == cudaSuccess;
+    ok &= dalloc(&w.segstart[b], (size_t)segcap + 4) == cudaSuccess;
+    ok &= dalloc(&w.tile_seg[b], max_tiles + 4) == cudaSuccess;
+  }
+  ok &= dalloc(&w.slots, (size_t)K * segcap + 4) == cudaSuccess;
+  ok &= dalloc(&w.lb_flag_round, max_tiles) == cudaSuccess;
+  ok &= dalloc(&w.lb_agg_round, max_tiles * 3) == cudaSuccess;
+  ok &= dalloc(&w.lb_incl_round, max_tiles * 3) == cudaSuccess;
+  ok &= dalloc(&w.lb_flag_book, book_tiles) == cudaSuccess;
+  ok &= dalloc(&w.lb_agg_book, book_tiles) == cudaSuccess;
+  ok &= dalloc(&w.lb_incl_book, book_tiles) == cudaSuccess;
+  ok &= dalloc(&w.vout, n + 8) == cudaSuccess;
+  w.red_blocks = (uint32_t)c->nsm * 2;
+  ok &= cudaMalloc((void**)&w.red, (size_t)w.red_blocks * 128 + 256) == cudaSuccess;
+  ok &= dalloc(&w.st, 1) == cudaSuccess;
+  if (ok && dim == 3) ok &= filter_alloc(c->fws, n) == 0;
+  if (!ok) {
+    free_ws(c);
+    cudaGetLastError();
+    return set_err(SH_NOMEM, "device allocation failed for the hull workspace");
+  }
+  CK(cudaMemset(w.slots, 0, ((size_t)K * segcap + 4) * sizeof(RunVal)));
+  CK(cudaMemset(w.lb_flag_round, 0, max_tiles * sizeof(uint64_t)));
+  CK(cudaMemset(w.lb_flag_book, 0, book_tiles * sizeof(uint64_t)));
+  CK(cudaMemset(w.st, 0, sizeof(DevState)));
+  w.max_tiles = (uint32_t)max_tiles;
+  w.round_grid = (uint32_t)(c->nsm * c->round_occ);
+  w.book_grid = (uint32_t)(c->nsm * c->book_occ);
+  c->dim = dim;
+  c->cap_n = n;
+  c->segcap = segcap;
+  return SH_OK;
+}
+
+static uint32_t default_segcap(int dim, uint64_t n) {
+  uint64_t s = std::max<uint64_t>(1u << 16, n / 8);
+  s = std::min<uint64_t>(s, n + 4);
+  return (uint32_t)s;
+}
+
+static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min) {
+  uint32_t want = std::max(default_segcap(dim, n), segcap_min);
+  if (c->dim == dim && c->cap_n >= n && c->segcap >= want) return SH_OK;
+  uint64_t cap = std::max<uint64_t>(n, (c->dim == dim) ? c->cap_n : 0);
+  return alloc_ws(c, dim, cap, std::max(want, (c->dim == dim) ? c->segcap : 0u));
+}
+
+// ---------------------------------------------------------------- graph
+template <int DIM>
+static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
+  size_t dsm = RoundSmem<DIM>::bytes();
+  k_round<DIM, false><<<ws.round_grid, BLOCK, dsm, s>>>(ws);
+  CK(cudaGetLastError());
+  k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+template <int DIM>
+static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
+  size_t dsm = RoundSmem<DIM>::bytes();
+  k_init<DIM><<<1, 32, 0, s>>>(ws);
+  CK(cudaGetLastError());
+  k_first_reduce<DIM><<<ws.red_blocks, BLOCK, 0, s>>>(ws);
+  CK(cudaGetLastError());
+  if (DIM == 3) {
+    k_line_far<<<ws.red_blocks, BLOCK, 0, s>>>(ws);
+    CK(cudaGetLastError());
+  }
+  k_round<DIM, true><<<ws.round_grid, BLOCK, dsm, s>>>(ws);
+  CK(cudaGetLastError());
+  k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+template <int DIM>
+static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
+  if (DIM == 3) {
+    int rc = filter_launch(c->fws, ws, c->nsm, s);
+    if (rc) return rc;
+  }
+  k_output<DIM><<<c->nsm * 4, BLOCK, 0, s>>>(ws, c->fws);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+template <int DIM>
+static int build_graph(sh_ctx* c) {
+  Graph& G = c->g[DIM];
+  if (G.exec) return SH_OK;
+  cudaStream_t s = c->build_stream;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t cg = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &ndeps));
+  cudaGraphConditionalHandle handle;
+  CK(cudaGraphConditionalHandleCreate(&handle, cg, 0, cudaGraphCondAssignDefault));
+  Workspace ws = c->ws;
+  ws.cond = handle;
+  ws.use_cond = 1;
+  int rc = launch_pre<DIM>(c, ws, s);
+  if (rc) {
+    cudaGraph_t tmp;
+    cudaStreamEndCapture(s, &tmp);
+    if (tmp) cudaGraphDestroy(tmp);
+    return rc;
+  }
+  CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &ndeps));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  CK(cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+  rc = launch_post<DIM>(c, ws, s);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &graph);
+  if (rc) return rc;
+  CK(e);
+  // loop body
+  CK(cudaStreamBeginCaptureToGraph(c->body_stream, body, nullptr, nullptr, 0,
+                                   cudaStreamCaptureModeThreadLocal));
+  rc = launch_body<DIM>(c, ws, c->body_stream);
+  cudaGraph_t bg = nullptr;
+  e = cudaStreamEndCapture(c->body_stream, &bg);
+  if (rc) return rc;
+  CK(e);
+  CK(cudaGraphInstantiate(&G.exec, graph, 0));
+  G.graph = graph;
+  return SH_OK;
+}
+
+template <int DIM>
+static int hull_async(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
+                      int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* facets,
+                      int64_t facet_cap, cudaStream_t s, uint32_t segcap_min) {
+  if (n <= 0) return set_err(SH_EMPTY, "cannot take the hull of an empty point set");
+  if (n >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "n must be < 2^31");
+  if (!x || !y || (DIM == 3 && !z) || !out_idx) return set_err(SH_CONTRACT, "null pointer");
+  if (stride < 1) return set_err(SH_CONTRACT, "stride must be >= 1");
+  if (!(eps_rel >= 0)) return set_err(SH_CONTRACT, "eps_rel must be nonnegative");
+  CK(cudaSetDevice(c->device));
+  int rc = ensure_ws(c, DIM, (uint64_t)n, segcap_min);
+  if (rc) return rc;
+  rc = build_graph<DIM>(c);
+  if (rc) return rc;
+  // call parameters -> device (pinned mirror, one small async copy)
+  DevState* h = c->st_host;
+  h->px = x;
+  h->py = y;
+  h->pz = (DIM == 3) ? z : y;
+  h->stride = stride;
+  h->n = (uint32_t)n;
+  h->dim = DIM;
+  h->eps_rel = eps_rel;
+  h->use_eps_abs = std::isnan(eps_abs) ? 0u : 1u;
+  h->eps_abs = std::isnan(eps_abs) ? 0.0 : eps_abs;
+  h->segcap = c->segcap;
+  h->out_idx = out_idx;
+  c->fws.out_facets = facets;
+  c->fws.facet_cap = facet_cap;
+  CK(cudaMemcpyAsync(c->ws.st, h, offsetof(DevState, eps), cudaMemcpyHostToDevice, s));
+  if (DIM == 3) {
+    int frc = filter_set_params(c->fws, facets, facet_cap, s);
+    if (frc) return frc;
+  }
+  CK(cudaGraphLaunch(c->g[DIM].exec, s));
+  c->last_n = (uint32_t)n;
+  return SH_OK;
+}
+
+static int fetch(sh_ctx* c, sh_result* res, cudaStream_t s) {
+  CK(cudaMemcpyAsync(c->st_host, c->ws.st, offsetof(DevState, tr_live), cudaMemcpyDeviceToHost, s));
+  uint64_t fres[4] = {0, 0, 0, 0};
+  if (c->dim == 3) CK(cudaMemcpyAsync(fres, c->fws.result, sizeof(fres), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const DevState* h = c->st_host;
+  if (res) {
+    memset(res, 0, sizeof(*res));
+    res->status = (int32_t)h->status;
+    res->flags = (int32_t)h->flags;
+    res->iterations = h->rounds_final;
+    res->eps = h->eps;
+    res->h = h->h_final;
+    res->candidates = h->h_final;
+    if (c->dim == 3) {
+      res->h = (int64_t)fres[0];
+      res->pruned = (int64_t)h->h_final - (int64_t)fres[0];
+      res->facets = (int64_t)fres[1];
+    }
+  }
+  if (h->status == ST_SEG_OVERFLOW) return SH_OK;  // caller retries
+  if (h->status == ST_DEGENERATE)
+    return set_err(SH_DEGENERATE, "all points are coplanar; project to the plane and use the 2D driver");
+  if (h->status == ST_ROUND_GUARD) return set_err(SH_ROUND_GUARD, "round count exceeded the input size");
+  return SH_OK;
+}
+
+template <int DIM>
+static int hull_sync(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
+                     int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* facets,
+                     int64_t facet_cap, sh_result* res, cudaStream_t s) {
+  uint32_t segmin = 0;
+  for (int attempt = 0; attempt < 8; attempt++) {
+    int rc = hull_async<DIM>(c, x, y, z, stride, n, eps_rel, eps_abs, out_idx, facets, facet_cap, s,
+                             segmin);
+    if (rc) return rc;
+    rc = fetch(c, res, s);
+    if (c->st_host->status != ST_SEG_OVERFLOW) return rc;
+    uint64_t need = (uint64_t)c->st_host->seg_needed * 2 + 1024;
+    segmin = (uint32_t)std::min<uint64_t>(need, (uint64_t)n + 4);
+  }
+  return set_err(SH_NOMEM, "segment table capacity retries exhausted");
+}
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+int sh_create(int device, sh_ctx** out) {
+  if (!out) return set_err(SH_CONTRACT, "null out pointer");
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_err(SH_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  sh_ctx* c = new sh_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  cudaFuncSetAttribute(k_round<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)RoundSmem<2>::bytes());
+  cudaFuncSetAttribute(k_round<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)RoundSmem<2>::bytes());
+  cudaFuncSetAttribute(k_round<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)RoundSmem<3>::bytes());
+  cudaFuncSetAttribute(k_round<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)RoundSmem<3>::bytes());
+  int o2 = 0, o3 = 0, ob = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_round<2, false>, BLOCK, RoundSmem<2>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_round<3, false>, BLOCK, RoundSmem<3>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
+  // one occupancy for both dims keeps the grids persistent for either
+  c->round_occ = std::max(1, std::min(o2, o3));
+  c->book_occ = std::max(1, std::min(ob, 4));
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    delete c;
+    return set_err(SH_CUDA, std::string("kernel setup: ") + cudaGetErrorString(e));
+  }
+  cudaStreamCreateWithFlags(&c->build_stream, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->body_stream, cudaStreamNonBlocking);
+  if (cudaMallocHost((void**)&c->st_host, sizeof(DevState)) != cudaSuccess) {
+    delete c;
+    return set_err(SH_NOMEM, "pinned allocation failed");
+  }
+  memset(c->st_host, 0, sizeof(DevState));
+  *out = c;
+  return SH_OK;
+}
+
+void sh_destroy(sh_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  free_ws(c);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->build_stream) cudaStreamDestroy(c->build_stream);
+  if (c->body_stream) cudaStreamDestroy(c->body_stream);
+  delete c;
+}
+
+int sh_reserve(sh_ctx* c, int dim, int64_t n) {
+  if (!c || (dim != 2 && dim != 3) || n <= 0) return set_err(SH_CONTRACT, "bad reserve arguments");
+  CK(cudaSetDevice(c->device));
+  int rc = ensure_ws(c, dim, (uint64_t)n, 0);
+  if (rc) return rc;
+  return dim == 2 ? build_graph<2>(c) : build_graph<3>(c);
+}
+
+int sh_hull2d(sh_ctx* c, const double* x, const double* y, int64_t stride, int64_t n, double eps_rel,
+              double eps_abs, int64_t* out_idx, sh_result* res, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  return hull_sync<2>(c, x, y, nullptr, stride, n, eps_rel, eps_abs, out_idx, nullptr, 0, res,
+                      (cudaStream_t)stream);
+}
+
+int sh_hull3d(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride, int64_t n,
+              double eps_rel, double eps_abs, int64_t* out_idx, int32_t* out_facets, int64_t facet_cap,
+              sh_result* res, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  return hull_sync<3>(c, x, y, z, stride, n, eps_rel, eps_abs, out_idx, out_facets, facet_cap, res,
+                      (cudaStream_t)stream);
+}
+
+int sh_hull2d_async(sh_ctx* c, const double* x, const double* y, int64_t stride, int64_t n,
+                    double eps_rel, double eps_abs, int64_t* out_idx, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  return hull_async<2>(c, x, y, nullptr, stride, n, eps_rel, eps_abs, out_idx, nullptr, 0,
+                       (cudaStream_t)stream, 0);
+}
+
+int sh_hull3d_async(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
+                    int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* out_facets,
+                    int64_t facet_cap, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  return hull_async<3>(c, x, y, z, stride, n, eps_rel, eps_abs, out_idx, out_facets, facet_cap,
+                       (cudaStream_t)stream, 0);
+}
+
+int sh_fetch(sh_ctx* c, sh_result* res, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  int rc = fetch(c, res, (cudaStream_t)stream);
+  if (c->st_host->status == ST_SEG_OVERFLOW)
+    return set_err(SH_NOMEM, "segment table overflow; use the synchronous call (it retries)");
+  return rc;
+}
+
+int64_t sh_trace(sh_ctx* c, int64_t* live, int64_t* kept, int64_t* nseg, int64_t* flat, int64_t cap) {
+  if (!c || !c->ws.st) return 0;
+  static_assert(offsetof(DevState, tr_flat) > offsetof(DevState, tr_live), "layout");
+  DevState* h = c->st_host;
+  if (cudaMemcpy(h, c->ws.st, sizeof(DevState), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  int64_t r = std::min<int64_t>(std::min<int64_t>(h->rounds_final, MAX_TRACE), cap);
+  for (int64_t i = 0; i < r; i++) {
+    if (live) live[i] = h->tr_live[i];
+    if (kept) kept[i] = h->tr_kept[i];
+    if (nseg) nseg[i] = h->tr_nseg[i];
+    if (flat) flat[i] = (c->dim == 3) ? h->tr_flat[i] : 0;
+  }
+  return r;
+}
+
+void sh_hypot_host(const double* x, const double* y, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; i++) out[i] = sh::glibc_hypot(x[i], y[i]);
+}
+
+const char* sh_last_error(void) { return g_last_error.c_str(); }
+const char* sh_version(void) { return "seghull_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

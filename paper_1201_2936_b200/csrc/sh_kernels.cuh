@@ -1,0 +1,293 @@
+// Kernels of the B200 Quickhull path (2D and 3D), see DESIGN.md.
+//
+//   K0  k_first_reduce  bbox (-> eps, Tolerance.effective geometry.py:79-83)
+//                       + lexicographic extremes (_lex_extreme quickhull.py:75-84)
+//   K0b k_line_far      3D third corner: farthest from the extrema line
+//                       (quickhull.py:329-344)
+//   K1  k_round<FIRST>  first split (quickhull.py:200-222 / :346-364)
+//   K2  k_round         one Quickhull round (quickhull.py:224-266 / :366-437):
+//                       simplex discard + child classification + stable
+//                       regroup into K streams + next round's segmented
+//                       farthest point, in ONE read and ONE write of the
+//                       live records, with a decoupled look-back scan that
+//                       carries both the stream offsets and the
+//                       reduce-by-key state of the farthest-point search.
+//   K3  k_book          per-segment bookkeeping (quickhull.py:236-240,
+//                       :268-277 / :380-391, :412-444): dense renumbering
+//                       of occupied children, child edge / face tables,
+//                       vertex emission, device-side termination flag.
+#pragma once
+
+#include "sh_common.cuh"
+
+namespace sh {
+
+// ------------------------------------------------------------------ K0
+struct LexRec {
+  double c[3];
+  uint32_t idx;
+  uint32_t pad;
+};
+
+template <int DIM>
+__device__ __forceinline__ bool lex_less(const LexRec& a, const LexRec& b) {
+  // a < b over (coords..., idx); fp comparisons, so -0.0 == +0.0 like
+  // `vals == best` in _lex_extreme.
+#pragma unroll
+  for (int k = 0; k < DIM; k++) {
+    if (a.c[k] < b.c[k]) return true;
+    if (a.c[k] > b.c[k]) return false;
+  }
+  return a.idx < b.idx;
+}
+
+struct FirstRed {
+  double lo[3], hi[3];
+  LexRec mn, mx;  // lex-min (lowest idx among ties), lex-max (highest idx)
+};
+
+template <int DIM>
+__device__ __forceinline__ void fr_merge(FirstRed& a, const FirstRed& b) {
+#pragma unroll
+  for (int k = 0; k < DIM; k++) {
+    a.lo[k] = fmin(a.lo[k], b.lo[k]);
+    a.hi[k] = fmax(a.hi[k], b.hi[k]);
+  }
+  if (lex_less<DIM>(b.mn, a.mn)) a.mn = b.mn;
+  if (lex_less<DIM>(a.mx, b.mx)) a.mx = b.mx;
+}
+
+__device__ __forceinline__ FirstRed ld_cg_fr(const FirstRed* p) {
+  FirstRed r;
+  const double* s = reinterpret_cast<const double*>(p);
+  double* d = reinterpret_cast<double*>(&r);
+  for (int i = 0; i < (int)(sizeof(FirstRed) / 8); i++) d[i] = __ldcg(s + i);
+  return r;
+}
+
+template <class T>
+__device__ __forceinline__ T shfl_xor_t(T v, int m) {
+  T r;
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(&v);
+  uint32_t* d = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(T) / 4); i++) d[i] = __shfl_xor_sync(0xFFFFFFFFu, s[i], m);
+  return r;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
+  DevState* st = ws.st;
+  if (threadIdx.x == 0) {
+    uint32_t tag = st->seq + 1;
+    st->status = ST_OK;
+    st->flags = 0;
+    st->h_final = 0;
+    st->rounds_final = 0;
+    st->seg_needed = 0;
+    st->first_active = 0;
+    st->ctr_round = 0;
+    st->ctr_book = 0;
+    st->ctr_red = 0;
+    st->dmax_bits = 0;
+    st->rp.active = 0;
+    st->bp.active = 0;
+    st->bp.tag = tag;   // unused until K1 finalises
+    st->rp.tag = tag;   // tag of K1 (first k_round launch)
+    st->seq = tag;
+  }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
+  DevState* st = ws.st;
+  const uint32_t n = st->n;
+  const int64_t stride = st->stride;
+  const double* P[3] = {st->px, st->py, st->pz};
+  FirstRed r;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    r.lo[k] = INFINITY;
+    r.hi[k] = -INFINITY;
+    r.mn.c[k] = INFINITY;
+    r.mx.c[k] = -INFINITY;
+  }
+  r.mn.idx = 0xFFFFFFFFu;
+  r.mx.idx = 0;
+  r.mn.pad = r.mx.pad = 0;
+  for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
+    LexRec q;
+#pragma unroll
+    for (int k = 0; k < 3; k++) q.c[k] = (k < DIM) ? ld_coord(P[k], stride, i) : 0.0;
+    q.idx = i;
+    q.pad = 0;
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+      r.lo[k] = fmin(r.lo[k], q.c[k]);
+      r.hi[k] = fmax(r.hi[k], q.c[k]);
+    }
+    if (lex_less<DIM>(q, r.mn)) r.mn = q;
+    if (lex_less<DIM>(r.mx, q)) r.mx = q;
+  }
+  // block reduce
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    FirstRed o = shfl_xor_t(r, m);
+    fr_merge<DIM>(r, o);
+  }
+  __shared__ FirstRed s_w[WARPS];
+  __shared__ bool s_last;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_w[warp] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < WARPS; w++) fr_merge<DIM>(s_w[0], s_w[w]);
+    FirstRed* parts = reinterpret_cast<FirstRed*>(ws.red);
+    parts[blockIdx.x] = s_w[0];
+    __threadfence();
+    uint32_t done = atomicAdd(&st->ctr_red, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  const FirstRed* parts = reinterpret_cast<const FirstRed*>(ws.red);
+  FirstRed t = ld_cg_fr(parts);
+  for (uint32_t b = 1; b < gridDim.x; b++) {
+    FirstRed o = ld_cg_fr(parts + b);
+    fr_merge<DIM>(t, o);
+  }
+  st->ctr_red = 0;
+  // Tolerance.effective: eps_rel * np.hypot.reduce(spans)
+  double acc = sub(t.hi[0], t.lo[0]);
+#pragma unroll
+  for (int k = 1; k < DIM; k++) acc = glibc_hypot(acc, sub(t.hi[k], t.lo[k]));
+  double eps = st->use_eps_abs ? st->eps_abs : mul(st->eps_rel, acc);
+  st->eps = eps;
+  st->imin = t.mn.idx;
+  st->imax = t.mx.idx;
+  bool same = true;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    st->pa[k] = t.mn.c[k];
+    st->pb[k] = t.mx.c[k];
+    if (k < DIM) same = same && (t.mn.c[k] == t.mx.c[k]);
+  }
+  ws.vout[0] = t.mn.idx;
+  if (same) {  // quickhull.py:195-197 / :320-322 -- every point coincides
+    st->h_final = 1;
+    return;
+  }
+  ws.vout[1] = t.mx.idx;
+  st->h_final = 2;
+  if (DIM == 2) {
+    // off_line threshold eps * edge_length(pmin, pmax), quickhull.py:203
+    st->thr_line = mul(eps, edge_length(t.mn.c[0], t.mn.c[1], t.mx.c[0], t.mx.c[1]));
+    st->first_active = 1;
+  } else {
+    st->first_active = (n > 2) ? 2u : 0u;  // 2: K0b runs next
+  }
+}
+
+// ------------------------------------------------------------------ K0b
+struct KeyIdx {
+  uint64_t hi;
+  uint32_t idx;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ bool ki_better(const KeyIdx& a, const KeyIdx& b) {
+  return (a.hi > b.hi) || (a.hi == b.hi && a.idx < b.idx);
+}
+
+__global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
+  DevState* st = ws.st;
+  if (st->first_active != 2) return;
+  const uint32_t n = st->n;
+  const int64_t stride = st->stride;
+  const double pa0 = st->pa[0], pa1 = st->pa[1], pa2 = st->pa[2];
+  const double ux = sub(st->pb[0], pa0), uy = sub(st->pb[1], pa1), uz = sub(st->pb[2], pa2);
+  const uint32_t imin = st->imin, imax = st->imax;
+  KeyIdx best;
+  best.hi = 0;
+  best.idx = 0xFFFFFFFFu;
+  best.pad = 0;
+  for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
+    if (i == imin || i == imax) continue;
+    double x = ld_coord(st->px, stride, i), y = ld_coord(st->py, stride, i),
+           z = ld_coord(st->pz, stride, i);
+    double cx, cy, cz;
+    // quickhull.py:331-334: cross3(q - pa, u), squared norm left to right
+    cross3(sub(x, pa0), sub(y, pa1), sub(z, pa2), ux, uy, uz, &cx, &cy, &cz);
+    double d2 = add(add(mul(cx, cx), mul(cy, cy)), mul(cz, cz));
+    KeyIdx k;
+    k.hi = ordered_bits(d2);
+    k.idx = i;
+    k.pad = 0;
+    if (ki_better(k, best)) best = k;
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    KeyIdx o = shfl_xor_t(best, m);
+    if (ki_better(o, best)) best = o;
+  }
+  __shared__ KeyIdx s_w[WARPS];
+  __shared__ bool s_last;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_w[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < WARPS; w++)
+      if (ki_better(s_w[w], s_w[0])) s_w[0] = s_w[w];
+    KeyIdx* parts = reinterpret_cast<KeyIdx*>(ws.red);
+    parts[blockIdx.x] = s_w[0];
+    __threadfence();
+    uint32_t done = atomicAdd(&st->ctr_red, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  const KeyIdx* parts = reinterpret_cast<const KeyIdx*>(ws.red);
+  KeyIdx t = parts[0];
+  for (uint32_t b = 1; b < gridDim.x; b++) {
+    KeyIdx o;
+    o.hi = __ldcg(&parts[b].hi);
+    o.idx = __ldcg(&parts[b].idx);
+    if (ki_better(o, t)) t = o;
+  }
+  st->ctr_red = 0;
+  const double eps = st->eps;
+  double d2 = from_ordered_bits(t.hi);
+  // np.linalg.norm(pb - pa) == sqrt(ddot(u, u)), OpenBLAS FMA order
+  double line_len = sqrt_(__fma_rn(uz, uz, __fma_rn(uy, uy, mul(ux, ux))));
+  if (sqrt_(d2) <= mul(eps, line_len)) {  // quickhull.py:337-339
+    st->flags |= FL_COLLINEAR;
+    st->first_active = 0;
+    return;
+  }
+  uint32_t f = t.idx;
+  st->ifar = f;
+  double pc[3] = {ld_coord(st->px, stride, f), ld_coord(st->py, stride, f),
+                  ld_coord(st->pz, stride, f)};
+  for (int k = 0; k < 3; k++) st->pc[k] = pc[k];
+  ws.vout[2] = f;
+  st->h_final = 3;
+  if (n == 3) {  // quickhull.py:343-344
+    st->first_active = 0;
+    return;
+  }
+  double nx, ny, nz;  // quickhull.py:346-347
+  cross3(sub(st->pb[0], pa0), sub(st->pb[1], pa1), sub(st->pb[2], pa2), sub(pc[0], pa0),
+         sub(pc[1], pa1), sub(pc[2], pa2), &nx, &ny, &nz);
+  st->nrm[0] = nx;
+  st->nrm[1] = ny;
+  st->nrm[2] = nz;
+  double nv[3] = {nx, ny, nz};
+  double nlen = norm3(nv);
+  st->nlen = nlen;
+  st->thr_line = mul(-eps, nlen);  // states = d < -eps * nlen (:353)
+  st->first_active = 1;
+}
+
+}  // namespace sh

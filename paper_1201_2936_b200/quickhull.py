@@ -1,0 +1,189 @@
+"""Drop-in hull entry points backed by the sm_100a CUDA path.
+
+Mirrors the reference drivers' public interface
+(/root/reference/pkg/src/seghull/quickhull.py):
+
+  quickhull_2d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult   (:167)
+  quickhull_3d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult   (:282)
+  HullResult(vertices, iterations, discarded, warnings)                         (:34-46)
+
+with the same exceptions (ContractViolation for a dimension mismatch,
+EmptyInputError for n = 0, DegenerateInputError for coplanar 3D input,
+AssertionError for the round guard) and the same warning strings.  The
+vertex coordinates come back in discovery order (first-split extremes, then
+round by round); the vertex SET is bit-exact with the reference.
+
+Index-returning variants work on device tensors without a host round trip:
+
+  hull_indices_2d(points) -> int64 CUDA tensor of original point indices
+  hull_indices_3d(points) -> (indices, facets or None)
+
+Every call goes through the C ABI (include/seghull_b200.h) into one CUDA
+graph launch; there is no CPU fallback.
+"""
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ContractViolation, DegenerateInputError, EmptyInputError
+from .geometry import PointSet, Tolerance
+
+
+@dataclass
+class HullResult:
+    """Hull vertex set plus run statistics (reference quickhull.py:34-46).
+
+    ``indices`` (not in the reference) holds the original indices of the
+    vertices; ``vertices`` their coordinates in the same order."""
+
+    vertices: PointSet
+    iterations: int
+    discarded: int
+    warnings: list = field(default_factory=list)
+    indices: np.ndarray = None
+
+
+def _raise_for(rc: int):
+    msg = _lib.last_error()
+    if rc == _lib.SH_CONTRACT:
+        raise ContractViolation(msg)
+    if rc == _lib.SH_EMPTY:
+        raise EmptyInputError(msg)
+    if rc == _lib.SH_DEGENERATE:
+        raise DegenerateInputError(msg)
+    if rc == _lib.SH_ROUND_GUARD:
+        raise AssertionError(msg)
+    raise RuntimeError(f"seghull_b200 error {rc}: {msg}")
+
+
+def _as_device_coords(points, dim):
+    """(n, dim) fp64 CUDA tensor (any row stride with unit column stride) or
+    a tuple of dim 1-D fp64 CUDA tensors -> (pointers, stride, n, keepalive)."""
+    if isinstance(points, (tuple, list)):
+        if len(points) != dim:
+            raise ContractViolation(f"expected {dim}D points, got {len(points)}D")
+        cols = []
+        for c in points:
+            if not (torch.is_tensor(c) and c.is_cuda and c.dtype == torch.float64 and c.dim() == 1):
+                raise ContractViolation("coordinate tensors must be 1-D float64 CUDA tensors")
+            cols.append(c.contiguous())
+        n = cols[0].numel()
+        if any(c.numel() != n for c in cols):
+            raise ContractViolation("coordinate arrays must be equal length")
+        return [c.data_ptr() for c in cols], 1, n, cols
+    t = points
+    if not (torch.is_tensor(t) and t.is_cuda and t.dtype == torch.float64 and t.dim() == 2):
+        raise ContractViolation("points must be an (n, dim) float64 CUDA tensor")
+    if t.shape[1] != dim:
+        raise ContractViolation(f"expected {dim}D points, got {t.shape[1]}D")
+    if t.stride(1) != 1:
+        t = t.contiguous()
+    n = t.shape[0]
+    base = t.data_ptr()
+    return [base + 8 * k for k in range(dim)], t.stride(0), n, [t]
+
+
+def _stream_ptr(device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False):
+    """Original indices (int64 CUDA tensor) of the 2D hull vertices."""
+    ptrs, stride, n, keep = _as_device_coords(points, 2)
+    device = keep[0].device.index
+    if n == 0:
+        raise EmptyInputError("cannot take the hull of an empty point set")
+    out = torch.empty(n, dtype=torch.int64, device=keep[0].device)
+    res = _lib.ShResult()
+    with torch.cuda.device(device):
+        rc = _lib.lib().sh_hull2d(_lib.context(device), ptrs[0], ptrs[1], stride, n, tol.eps_rel,
+                                  tol.eps_abs, out.data_ptr(), ctypes.byref(res), _stream_ptr(device))
+    if rc != _lib.SH_OK:
+        _raise_for(rc)
+    idx = out[:res.h]
+    return (idx, res) if return_info else idx
+
+
+def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False):
+    """Original indices (int64 CUDA tensor) of the 3D hull vertices, plus the
+    (f, 3) int32 facet triples when ``facets`` is true."""
+    ptrs, stride, n, keep = _as_device_coords(points, 3)
+    device = keep[0].device.index
+    if n == 0:
+        raise EmptyInputError("cannot take the hull of an empty point set")
+    out = torch.empty(n, dtype=torch.int64, device=keep[0].device)
+    fcap = 2 * n + 8 if facets else 0
+    fout = torch.empty((max(fcap, 1), 3), dtype=torch.int32, device=keep[0].device)
+    res = _lib.ShResult()
+    with torch.cuda.device(device):
+        rc = _lib.lib().sh_hull3d(_lib.context(device), ptrs[0], ptrs[1], ptrs[2], stride, n,
+                                  tol.eps_rel, tol.eps_abs, out.data_ptr(),
+                                  fout.data_ptr() if facets else None, fcap, ctypes.byref(res),
+                                  _stream_ptr(device))
+    if rc != _lib.SH_OK:
+        _raise_for(rc)
+    idx = out[:res.h]
+    fac = fout[:res.facets] if facets else None
+    if return_info:
+        return idx, fac, res
+    return (idx, fac) if facets else idx
+
+
+def trace(device=None):
+    """Per-round counters of the last hull on ``device``: rows of (live points
+    entering, survivors, segments, near-coplanar segments dropped)."""
+    device = torch.cuda.current_device() if device is None else device
+    cap = 4096
+    arrs = [np.zeros(cap, np.int64) for _ in range(4)]
+    r = _lib.lib().sh_trace(_lib.context(device), *(a.ctypes.data for a in arrs), cap)
+    return np.stack([a[:r] for a in arrs], axis=1)
+
+
+def _validate(points: PointSet, dim: int):
+    # quickhull.py:103-107
+    if points.dim != dim:
+        raise ContractViolation(f"expected {dim}D points, got {points.dim}D")
+    if points.n == 0:
+        raise EmptyInputError("cannot take the hull of an empty point set")
+
+
+def _to_device(points: PointSet):
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return tuple(torch.from_numpy(c).to(dev, non_blocking=False) for c in points.coords)
+
+
+def quickhull_2d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
+    """Strict 2D hull (reference quickhull.py:167-279), computed on the GPU."""
+    _validate(points, 2)
+    cols = _to_device(points)
+    idx, res = hull_indices_2d(cols, tol, return_info=True)
+    idx = idx.cpu().numpy()
+    verts = PointSet(tuple(c[idx] for c in points.coords))
+    warnings = []
+    if res.flags & _lib.SH_FLAG_COLLINEAR:
+        warnings.append("collinear input: hull is the two x-extrema")  # :208
+    return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx)
+
+
+def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
+    """3D hull vertex set (reference quickhull.py:282-446), computed on the GPU."""
+    _validate(points, 3)
+    cols = _to_device(points)
+    idx, _, res = hull_indices_3d(cols, tol, return_info=True)
+    idx = idx.cpu().numpy()
+    warnings = []
+    if res.flags & _lib.SH_FLAG_COLLINEAR:
+        warnings.append("collinear input: hull is the two extrema")  # :338
+    if res.iterations:
+        for r, (_, _, _, flat) in enumerate(trace(cols[0].device.index), start=1):
+            if flat:
+                warnings.append(f"round {r}: dropped {int(flat)} near-coplanar segment(s)")  # :387-389
+    if res.pruned:
+        warnings.append(f"pruned {int(res.pruned)} non-extreme candidate vertex(es) emitted by "
+                        "incomplete per-face outside sets")  # :308-310
+    verts = PointSet(tuple(c[idx] for c in points.coords)) if idx.size else PointSet.empty(3)
+    return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx)
