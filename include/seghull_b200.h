@@ -98,6 +98,11 @@ int sh_reserve(sh_ctx* ctx, int dim, int64_t n);
  * lengths (no GPU needed). */
 void sh_hypot_host(const double* x, const double* y, double* out, int64_t n);
 
+/* 0 (default): one CUDA-graph launch per hull, round loop on the device.
+ * 1: host-driven round loop (one sync per round) -- for profilers that can
+ * not attribute kernels inside conditional graphs. */
+int sh_set_launch_mode(sh_ctx* ctx, int mode);
+
 const char* sh_last_error(void);
 const char* sh_version(void);
 

@@ -27,7 +27,7 @@ struct BookShared {
   uint32_t tile;
   uint32_t wsum[ITEMS3 * WARPS * 3];
   Sum3 agg, prefix;
-  Sum3 window[32];
+  int stop[4];
 };
 
 template <int DIM>
@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
   const uint32_t E = K * nsp;
   const uint32_t num_tiles = (E + TILE3 - 1) / TILE3;
   const uint32_t tag = bp.tag;
+  const uint32_t tag16 = (tag % 65535u) + 1u;
   const double eps = st->eps;
   const uint32_t segcap = st->segcap;
   const int64_t stride = st->stride;
@@ -72,13 +73,16 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       v[j].idx = 0;
       v[j].cnt = 0;
       if (e < E) {
-        v[j] = ld_cg(&ws.slots[e]);
+        v[j].cnt = __ldcg(&ws.slot_cnt[e]);
         if (v[j].cnt) {
-          RunVal z;
+          Key128 k = ld_cg(&ws.slot_key[e]);
+          v[j].hi = k.hi;
+          v[j].idx = (uint32_t)k.lo;
+          Key128 z;
           z.hi = 0;
-          z.idx = 0;
-          z.cnt = 0;
-          st_cg(&ws.slots[e], z);  // slots are all-zero between uses
+          z.lo = 0;
+          st_cg(&ws.slot_key[e], z);  // slots are all-zero between uses
+          __stcg(&ws.slot_cnt[e], 0u);
         }
       }
       bool occ = v[j].cnt > 0;
@@ -129,7 +133,6 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
     }
     __syncthreads();
     if (warp == 0) {
-      Sum3 a;
 #pragma unroll
       for (int q = 0; q < 3; q++) {
         uint32_t w = sb.wsum[lane * 3 + q];
@@ -140,28 +143,22 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
           if (lane >= off) x += o;
         }
         sb.wsum[lane * 3 + q] = x - w;
-        a.v[q] = __shfl_sync(0xFFFFFFFFu, x, 31);
-      }
-      a.v[3] = 0;
-      Sum3 pre = s3_identity();
-      if (tile == 0) {
-        lookback_publish_incl<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_incl_book, tile,
-                                                                tag, &a);
-      } else {
-        lookback_publish_agg<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_agg_book, tile,
-                                                               tag, &a);
-        lookback_wait<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_agg_book,
-                                                        ws.lb_incl_book, tile, tag, sb.window, &pre);
-        Sum3 inc = s3_combine(pre, a);
-        lookback_publish_incl<Sum3, 1, s3_identity, s3_combine>(ws.lb_flag_book, ws.lb_incl_book, tile,
-                                                                tag, &inc);
-      }
-      if (lane == 0) {
-        sb.prefix = pre;
-        sb.agg = a;
+        uint32_t tot = __shfl_sync(0xFFFFFFFFu, x, 31);
+        if (lane == 0) sb.agg.v[q] = tot;
       }
     }
     __syncthreads();
+    if (tile > 0) {
+      if (tid == 0) lb_publish<3>(ws.lb_book, tile, tag16, LB_AGG, sb.agg.v);
+      lb_lookback<3>(ws.lb_book, tile, tag16, sb.prefix.v, sb.stop);
+    } else if (tid < 3) {
+      sb.prefix.v[tid] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      Sum3 inc = s3_combine(sb.prefix, sb.agg);
+      lb_publish<3>(ws.lb_book, tile, tag16, LB_INC, inc.v);
+    }
 
     // ---- build child tables, emit vertices
 #pragma unroll

@@ -43,6 +43,13 @@ constexpr uint32_t FL_COLLINEAR = 1;
 // Larger `hi` (order-preserving bits of the distance) wins, ties go to the
 // lowest original index (quickhull.py:93-100: first max in a segment whose
 // elements are in ascending original-index order).  cnt sums.
+// 128-bit farthest-point key in a child slot: (hi, idx) with larger hi
+// winning and ties going to the lower index.
+struct __align__(16) Key128 {
+  unsigned long long hi;
+  unsigned long long lo;  // original index
+};
+
 struct __align__(16) RunVal {
   uint64_t hi;
   uint32_t idx;
@@ -205,14 +212,13 @@ struct Workspace {
   uint32_t* segstart[2];
   uint32_t* tile_seg[2];
   // child results, stream-order ids, zero between uses
-  RunVal* slots;
-  // decoupled look-back state
-  uint64_t* lb_flag_round;
-  StreamAgg* lb_agg_round;   // [tiles][4]
-  StreamAgg* lb_incl_round;
-  uint64_t* lb_flag_book;
-  Sum3* lb_agg_book;
-  Sum3* lb_incl_book;
+  Key128* slot_key;
+  uint32_t* slot_cnt;
+  // decoupled look-back status words, [tiles][4]
+  uint64_t* lb_round;
+  uint64_t* lb_book;
+  uint64_t lb_round_words;
+  uint64_t lb_book_words;
   // vertex output (uint32 original indices)
   uint32_t* vout;
   // reduction partials
@@ -320,6 +326,178 @@ __device__ void lookback_publish_incl(uint64_t* flags, P* incl, uint32_t tile, u
   __threadfence();
   __syncwarp();
   if (lane == 0) st_volatile_u64(&flags[tile], ((uint64_t)tag << 2) | 2ull);
+}
+
+// ------------------------------------------------------------------------
+// Count-only decoupled look-back (the hot-path variant).
+// One 64-bit status word per (tile, counter): [tag:16][flag:2][count:46].
+// The count travels inside the status word, so a reader needs exactly one
+// load per predecessor and no memory fence; every counter is an independent
+// chained scan.  Tags (1..65535, never 0) separate launches, the arrays are
+// zeroed at allocation and re-zeroed by k_init before the tag space wraps.
+constexpr uint64_t LB_AGG = 1, LB_INC = 2;
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t lb_word(uint32_t tag, uint64_t flag, uint32_t count) {
+  return ((uint64_t)tag << 48) | (flag << 46) | (uint64_t)count;
+}
+
+template <int NC>
+__device__ __forceinline__ void lb_publish(uint64_t* st, uint32_t tile, uint32_t tag, uint64_t flag,
+                                           const uint32_t* cnt) {
+#pragma unroll
+  for (int c = 0; c < NC; c++) st_relaxed_u64(&st[(size_t)tile * 4 + c], lb_word(tag, flag, cnt[c]));
+}
+
+// All threads of the block call this.  On return s_prefix[0..NC) holds the
+// exclusive prefix of `tile` for every counter.
+template <int NC>
+__device__ void lb_lookback(const uint64_t* st, uint32_t tile, uint32_t tag, uint32_t* s_prefix,
+                            int* s_stop) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = warp * 32 + lane;
+  if (threadIdx.x < NC) s_prefix[threadIdx.x] = 0;
+  bool done[NC];
+#pragma unroll
+  for (int c = 0; c < NC; c++) done[c] = false;
+  int64_t pos = (int64_t)tile - 1;
+  __syncthreads();
+  while (pos >= 0) {
+    const int64_t t = pos - g;
+    const bool valid = t >= 0;
+    uint64_t w[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      w[c] = 0;
+      if (valid && !done[c]) {
+        do {
+          w[c] = ld_relaxed_u64(&st[(size_t)t * 4 + c]);
+        } while ((uint32_t)(w[c] >> 48) != tag || ((w[c] >> 46) & 3ull) == 0);
+      }
+    }
+    if (threadIdx.x < NC) s_stop[threadIdx.x] = 1 << 30;
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      uint32_t im = __ballot_sync(0xFFFFFFFFu, valid && !done[c] && ((w[c] >> 46) & 3ull) == LB_INC);
+      if (lane == 0 && im) atomicMin(&s_stop[c], warp * 32 + (__ffs(im) - 1));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      const int stop = s_stop[c];
+      uint32_t v = (valid && !done[c] && g <= stop) ? (uint32_t)(w[c] & ((1ull << 46) - 1)) : 0u;
+      v = __reduce_add_sync(0xFFFFFFFFu, v);
+      if (lane == 0 && v) atomicAdd(&s_prefix[c], v);
+    }
+    bool all = true;
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+      done[c] = done[c] || (s_stop[c] < (1 << 30));
+      all = all && done[c];
+    }
+    __syncthreads();
+    if (all) break;
+    pos -= 32 * WARPS;
+  }
+}
+
+__device__ __forceinline__ void atomic_max_key(Key128* p, uint64_t hi, uint32_t idx) {
+  // cheap filter: the slot's hi only grows, so a smaller hi can never win
+  uint64_t cur_hi = ld_relaxed_u64(reinterpret_cast<const uint64_t*>(p));
+  if (hi < cur_hi) return;
+  Key128 want;
+  want.hi = hi;
+  want.lo = idx;
+  Key128 cmp;
+  cmp.hi = cur_hi;
+  cmp.lo = 0;
+  for (;;) {
+    Key128 old = atomicCAS(p, cmp, want);
+    if (old.hi == cmp.hi && old.lo == cmp.lo) return;
+    if (!(hi > old.hi || (hi == old.hi && (unsigned long long)idx < old.lo))) return;
+    cmp = old;
+  }
+}
+
+// Whole-block look-back: every warp inspects 32 predecessors, so one step
+// covers 32*WARPS tiles in about one L2 round trip.  (A single-warp window
+// caps the tile rate at 32 tiles per round trip, below what HBM needs at
+// 2048-point tiles.)  The window is reduced in parallel: a shuffle tree per
+// warp (older tiles on the left of COMBINE) and a short serial pass over
+// the warp results.  Must be called by all threads of the block; on return
+// s_prefix[0..NP) holds the exclusive prefix of `tile`.
+template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
+__device__ void lookback_block(const uint64_t* flags, const P* agg, const P* incl, uint32_t tile,
+                               uint32_t tag, P* s_warp /*[WARPS*NP]*/, P* s_prefix /*[NP]*/,
+                               int* s_ctl /*[2]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NP; i++) s_prefix[i] = IDENT();
+  }
+  int64_t pos = (int64_t)tile - 1;
+  while (pos >= 0) {
+    const int g = warp * 32 + lane;
+    const int64_t t = pos - g;
+    const bool valid = t >= 0;
+    uint32_t fl = 0;
+    if (valid) {
+      uint64_t w;
+      do {
+        w = ld_volatile_u64(&flags[t]);
+      } while ((w >> 2) != (uint64_t)tag || (w & 3ull) == 0);
+      fl = (uint32_t)(w & 3ull);
+    }
+    // nearest inclusive predecessor in the whole window
+    if (threadIdx.x == 0) s_ctl[0] = 1 << 30;
+    __syncthreads();
+    uint32_t im = __ballot_sync(0xFFFFFFFFu, valid && fl == 2);
+    if (lane == 0 && im) atomicMin(&s_ctl[0], warp * 32 + (__ffs(im) - 1));
+    __syncthreads();
+    const int gstop = s_ctl[0];
+    __threadfence();
+    P v[NP];
+    const bool use = valid && g <= gstop;
+#pragma unroll
+    for (int i = 0; i < NP; i++) {
+      v[i] = IDENT();
+      if (use) v[i] = ld_cg(&((fl == 2) ? incl : agg)[(size_t)t * NP + i]);
+    }
+    // shuffle tree: lane l ends with v[l] (+) ... combined over older lanes
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+      for (int i = 0; i < NP; i++) {
+        P o = shfl_down_t(v[i], off);
+        if (lane + off < 32) v[i] = COMBINE(o, v[i]);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NP; i++) s_warp[warp * NP + i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < NP; i++) {
+        P w = IDENT();
+        for (int ww = WARPS - 1; ww >= 0; ww--) w = COMBINE(w, s_warp[ww * NP + i]);
+        s_prefix[i] = COMBINE(w, s_prefix[i]);
+      }
+    }
+    __syncthreads();
+    if (gstop < (1 << 30)) break;
+    pos -= 32 * WARPS;
+  }
 }
 
 // window: shared scratch of 32*NP payloads.  On return prefix[0..NP) (all

@@ -52,6 +52,7 @@ struct sh_ctx {
   Graph g[4];
   int round_occ = 0, book_occ = 0;
   uint32_t last_n = 0;
+  int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop (profiling)
 };
 
 #define CK(x)                                                                     \
@@ -84,13 +85,10 @@ static void free_ws(sh_ctx* c) {
     cudaFree(w.segstart[b]);
     cudaFree(w.tile_seg[b]);
   }
-  cudaFree(w.slots);
-  cudaFree(w.lb_flag_round);
-  cudaFree(w.lb_agg_round);
-  cudaFree(w.lb_incl_round);
-  cudaFree(w.lb_flag_book);
-  cudaFree(w.lb_agg_book);
-  cudaFree(w.lb_incl_book);
+  cudaFree(w.slot_key);
+  cudaFree(w.slot_cnt);
+  cudaFree(w.lb_round);
+  cudaFree(w.lb_book);
   cudaFree(w.vout);
   cudaFree(w.red);
   cudaFree(w.st);
@@ -128,15 +126,14 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap) {
     ok &= dalloc(&w.segstart[b], (size_t)segcap + 4) == cudaSuccess;
     ok &= dalloc(&w.tile_seg[b], max_tiles + 4) == cudaSuccess;
   }
-  ok &= dalloc(&w.slots, (size_t)K * segcap + 4) == cudaSuccess;
-  ok &= dalloc(&w.lb_flag_round, max_tiles) == cudaSuccess;
-  ok &= dalloc(&w.lb_agg_round, max_tiles * 3) == cudaSuccess;
-  ok &= dalloc(&w.lb_incl_round, max_tiles * 3) == cudaSuccess;
-  ok &= dalloc(&w.lb_flag_book, book_tiles) == cudaSuccess;
-  ok &= dalloc(&w.lb_agg_book, book_tiles) == cudaSuccess;
-  ok &= dalloc(&w.lb_incl_book, book_tiles) == cudaSuccess;
+  ok &= dalloc(&w.slot_key, (size_t)K * segcap + 4) == cudaSuccess;
+  ok &= dalloc(&w.slot_cnt, (size_t)K * segcap + 4) == cudaSuccess;
+  ok &= dalloc(&w.lb_round, max_tiles * 4) == cudaSuccess;
+  ok &= dalloc(&w.lb_book, book_tiles * 4) == cudaSuccess;
+  w.lb_round_words = max_tiles * 4;
+  w.lb_book_words = book_tiles * 4;
   ok &= dalloc(&w.vout, n + 8) == cudaSuccess;
-  w.red_blocks = (uint32_t)c->nsm * 2;
+  w.red_blocks = (uint32_t)c->nsm * 8;
   ok &= cudaMalloc((void**)&w.red, (size_t)w.red_blocks * 128 + 256) == cudaSuccess;
   ok &= dalloc(&w.st, 1) == cudaSuccess;
   if (ok && dim == 3) ok &= filter_alloc(c->fws, n) == 0;
@@ -145,9 +142,10 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap) {
     cudaGetLastError();
     return set_err(SH_NOMEM, "device allocation failed for the hull workspace");
   }
-  CK(cudaMemset(w.slots, 0, ((size_t)K * segcap + 4) * sizeof(RunVal)));
-  CK(cudaMemset(w.lb_flag_round, 0, max_tiles * sizeof(uint64_t)));
-  CK(cudaMemset(w.lb_flag_book, 0, book_tiles * sizeof(uint64_t)));
+  CK(cudaMemset(w.slot_key, 0, ((size_t)K * segcap + 4) * sizeof(Key128)));
+  CK(cudaMemset(w.slot_cnt, 0, ((size_t)K * segcap + 4) * sizeof(uint32_t)));
+  CK(cudaMemset(w.lb_round, 0, max_tiles * 4 * sizeof(uint64_t)));
+  CK(cudaMemset(w.lb_book, 0, book_tiles * 4 * sizeof(uint64_t)));
   CK(cudaMemset(w.st, 0, sizeof(DevState)));
   w.max_tiles = (uint32_t)max_tiles;
   w.round_grid = (uint32_t)(c->nsm * c->round_occ);
@@ -185,7 +183,7 @@ static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
 template <int DIM>
 static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
-  k_init<DIM><<<1, 32, 0, s>>>(ws);
+  k_init<DIM><<<1, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   k_first_reduce<DIM><<<ws.red_blocks, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
@@ -296,7 +294,25 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     int frc = filter_set_params(c->fws, facets, facet_cap, s);
     if (frc) return frc;
   }
-  CK(cudaGraphLaunch(c->g[DIM].exec, s));
+  if (c->launch_mode == 0) {
+    CK(cudaGraphLaunch(c->g[DIM].exec, s));
+  } else {
+    // host-driven loop: same kernels, one host sync per round (ncu can not
+    // attribute kernels inside graphs that contain conditional nodes)
+    Workspace ws = c->ws;
+    ws.use_cond = 0;
+    rc = launch_pre<DIM>(c, ws, s);
+    if (rc) return rc;
+    for (;;) {
+      CK(cudaMemcpyAsync(&h->rp, &c->ws.st->rp, sizeof(RoundParams), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (!h->rp.active) break;
+      rc = launch_body<DIM>(c, ws, s);
+      if (rc) return rc;
+    }
+    rc = launch_post<DIM>(c, ws, s);
+    if (rc) return rc;
+  }
   c->last_n = (uint32_t)n;
   return SH_OK;
 }
@@ -460,6 +476,12 @@ int64_t sh_trace(sh_ctx* c, int64_t* live, int64_t* kept, int64_t* nseg, int64_t
 
 void sh_hypot_host(const double* x, const double* y, double* out, int64_t n) {
   for (int64_t i = 0; i < n; i++) out[i] = sh::glibc_hypot(x[i], y[i]);
+}
+
+int sh_set_launch_mode(sh_ctx* c, int mode) {
+  if (!c || (mode != 0 && mode != 1)) return set_err(SH_CONTRACT, "mode must be 0 (graph) or 1 (host loop)");
+  c->launch_mode = mode;
+  return SH_OK;
 }
 
 const char* sh_last_error(void) { return g_last_error.c_str(); }

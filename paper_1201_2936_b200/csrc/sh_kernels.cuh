@@ -78,6 +78,16 @@ __device__ __forceinline__ T shfl_xor_t(T v, int m) {
 template <int DIM>
 __global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
   DevState* st = ws.st;
+  // Look-back status words carry a 16-bit launch tag; long before the tag
+  // space wraps, zero the status arrays and restart the tags.
+  if (st->seq % 65535u >= 32768u) {
+    for (uint64_t i = threadIdx.x; i < ws.lb_round_words; i += blockDim.x) ws.lb_round[i] = 0;
+    for (uint64_t i = threadIdx.x; i < ws.lb_book_words; i += blockDim.x) ws.lb_book[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) st->seq = 0;
+    __threadfence();
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     uint32_t tag = st->seq + 1;
     st->status = ST_OK;
@@ -115,12 +125,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   r.mn.idx = 0xFFFFFFFFu;
   r.mx.idx = 0;
   r.mn.pad = r.mx.pad = 0;
-  for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
-    LexRec q;
-#pragma unroll
-    for (int k = 0; k < 3; k++) q.c[k] = (k < DIM) ? ld_coord(P[k], stride, i) : 0.0;
-    q.idx = i;
-    q.pad = 0;
+  auto visit = [&](const LexRec& q) {
 #pragma unroll
     for (int k = 0; k < DIM; k++) {
       r.lo[k] = fmin(r.lo[k], q.c[k]);
@@ -128,6 +133,28 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     }
     if (lex_less<DIM>(q, r.mn)) r.mn = q;
     if (lex_less<DIM>(r.mx, q)) r.mx = q;
+  };
+  const uint32_t G = gridDim.x * BLOCK;
+  uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  for (; (uint64_t)i + 3ull * G < n; i += 4 * G) {  // 4 independent loads in flight
+    LexRec q[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+#pragma unroll
+      for (int k = 0; k < 3; k++) q[u].c[k] = (k < DIM) ? ld_coord(P[k], stride, i + u * G) : 0.0;
+      q[u].idx = i + u * G;
+      q[u].pad = 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) visit(q[u]);
+  }
+  for (; i < n; i += G) {
+    LexRec q;
+#pragma unroll
+    for (int k = 0; k < 3; k++) q.c[k] = (k < DIM) ? ld_coord(P[k], stride, i) : 0.0;
+    q.idx = i;
+    q.pad = 0;
+    visit(q);
   }
   // block reduce
 #pragma unroll
@@ -149,14 +176,31 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     s_last = (done == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
   __threadfence();
-  const FirstRed* parts = reinterpret_cast<const FirstRed*>(ws.red);
-  FirstRed t = ld_cg_fr(parts);
-  for (uint32_t b = 1; b < gridDim.x; b++) {
-    FirstRed o = ld_cg_fr(parts + b);
-    fr_merge<DIM>(t, o);
+  {  // last block: parallel reduction of the per-block partials
+    const FirstRed* parts = reinterpret_cast<const FirstRed*>(ws.red);
+    FirstRed t = r;
+    bool any = false;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+      FirstRed o = ld_cg_fr(parts + b);
+      if (!any) t = o;
+      else fr_merge<DIM>(t, o);
+      any = true;
+    }
+    if (!any) t = ld_cg_fr(parts);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      FirstRed o = shfl_xor_t(t, m);
+      fr_merge<DIM>(t, o);
+    }
+    __syncthreads();
+    if (lane == 0) s_w[warp] = t;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < WARPS; w++) fr_merge<DIM>(s_w[0], s_w[w]);
   }
+  const FirstRed t = s_w[0];
   st->ctr_red = 0;
   // Tolerance.effective: eps_rel * np.hypot.reduce(spans)
   double acc = sub(t.hi[0], t.lo[0]);
@@ -212,10 +256,8 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
   best.hi = 0;
   best.idx = 0xFFFFFFFFu;
   best.pad = 0;
-  for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
-    if (i == imin || i == imax) continue;
-    double x = ld_coord(st->px, stride, i), y = ld_coord(st->py, stride, i),
-           z = ld_coord(st->pz, stride, i);
+  auto visit = [&](uint32_t i, double x, double y, double z) {
+    if (i == imin || i == imax) return;
     double cx, cy, cz;
     // quickhull.py:331-334: cross3(q - pa, u), squared norm left to right
     cross3(sub(x, pa0), sub(y, pa1), sub(z, pa2), ux, uy, uz, &cx, &cy, &cz);
@@ -225,7 +267,22 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
     k.idx = i;
     k.pad = 0;
     if (ki_better(k, best)) best = k;
+  };
+  const uint32_t G = gridDim.x * BLOCK;
+  uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  for (; (uint64_t)i + 3ull * G < n; i += 4 * G) {
+    double x[4], y[4], z[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      x[u] = ld_coord(st->px, stride, i + u * G);
+      y[u] = ld_coord(st->py, stride, i + u * G);
+      z[u] = ld_coord(st->pz, stride, i + u * G);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) visit(i + u * G, x[u], y[u], z[u]);
   }
+  for (; i < n; i += G)
+    visit(i, ld_coord(st->px, stride, i), ld_coord(st->py, stride, i), ld_coord(st->pz, stride, i));
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {
     KeyIdx o = shfl_xor_t(best, m);
@@ -246,15 +303,32 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
     s_last = (done == gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
   __threadfence();
-  const KeyIdx* parts = reinterpret_cast<const KeyIdx*>(ws.red);
-  KeyIdx t = parts[0];
-  for (uint32_t b = 1; b < gridDim.x; b++) {
-    KeyIdx o;
-    o.hi = __ldcg(&parts[b].hi);
-    o.idx = __ldcg(&parts[b].idx);
-    if (ki_better(o, t)) t = o;
+  KeyIdx t;
+  {
+    const KeyIdx* parts = reinterpret_cast<const KeyIdx*>(ws.red);
+    t.hi = 0;
+    t.idx = 0xFFFFFFFFu;
+    t.pad = 0;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+      KeyIdx o;
+      o.hi = __ldcg(&parts[b].hi);
+      o.idx = __ldcg(&parts[b].idx);
+      o.pad = 0;
+      if (ki_better(o, t)) t = o;
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      KeyIdx o = shfl_xor_t(t, m);
+      if (ki_better(o, t)) t = o;
+    }
+    __syncthreads();
+    if (lane == 0) s_w[warp] = t;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 0; w < WARPS; w++)
+      if (ki_better(s_w[w], t)) t = s_w[w];
   }
   st->ctr_red = 0;
   const double eps = st->eps;

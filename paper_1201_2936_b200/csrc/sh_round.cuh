@@ -49,8 +49,12 @@ struct RoundShared {
   uint32_t wcnt[ITEMS * WARPS * 3];
   uint32_t fkey[3], lkey[3];
   RunVal first[3], last_run[3];
-  StreamAgg agg[3], prefix[3];
-  StreamAgg window[32 * 3];
+  uint32_t cnt[4], prefix[4], incl[4];
+  int stop[4];
+  // per-block pending run per stream, carried across the block's tiles
+  uint32_t pend_key[3];
+  uint32_t pend_valid[3];
+  RunVal pend[3];
   Frag frag[WARPS];
 };
 
@@ -63,8 +67,8 @@ __device__ __forceinline__ RunVal rv_ident() {
 }
 
 template <int K>
-__device__ __forceinline__ void flush_run(RoundShared& sh_, RunVal* slots, uint32_t nseg, uint32_t key,
-                                          RunVal v) {
+__device__ __forceinline__ void flush_run(RoundShared& sh_, const Workspace& ws, uint32_t nseg,
+                                          uint32_t key, RunVal v) {
   uint32_t s = (K == 1) ? 0 : key / nseg;
   bool done = false;
   if (key == sh_.fkey[s]) {
@@ -75,7 +79,33 @@ __device__ __forceinline__ void flush_run(RoundShared& sh_, RunVal* slots, uint3
     sh_.last_run[s] = v;
     done = true;
   }
-  if (!done) st_cg(&slots[key], v);  // complete run inside the tile: final
+  if (!done) {
+    // a run bounded by other keys inside the tile is the whole child
+    Key128 k;
+    k.hi = v.hi;
+    k.lo = v.idx;
+    st_cg(&ws.slot_key[key], k);
+    ws.slot_cnt[key] = v.cnt;
+  }
+}
+
+// Boundary runs of a child that spans tiles: merged with atomics.
+__device__ __forceinline__ void flush_atomic(const Workspace& ws, uint32_t key, RunVal v) {
+  atomicAdd(&ws.slot_cnt[key], v.cnt);
+  atomic_max_key(&ws.slot_key[key], v.hi, v.idx);
+}
+
+// Thread 0: fold a boundary run into the block's pending run of its stream.
+__device__ __forceinline__ void pend_push(RoundShared& sh_, const Workspace& ws, int s, uint32_t key,
+                                          RunVal v) {
+  if (sh_.pend_valid[s] && sh_.pend_key[s] == key) {
+    sh_.pend[s] = rv_merge(sh_.pend[s], v);
+  } else {
+    if (sh_.pend_valid[s]) flush_atomic(ws, sh_.pend_key[s], sh_.pend[s]);
+    sh_.pend_key[s] = key;
+    sh_.pend[s] = v;
+    sh_.pend_valid[s] = 1;
+  }
 }
 
 // Classification of one point against its segment (2D), quickhull.py:230-266.
@@ -185,6 +215,8 @@ __global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
     if (DIM == 3) f_ifar = st->ifar;
   }
   double dmax_local = 0.0;
+  const uint32_t tag16 = (tag % 65535u) + 1u;
+  if (tid < 3) sh_.pend_valid[tid] = 0;
 
   while (true) {
     if (tid == 0) sh_.tile = atomicAdd(&st->ctr_round, 1u);
@@ -398,9 +430,9 @@ __global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
             first_open = false;
           }
         } else if (closeA) {
-          if (lane == 0) flush_run<K>(sh_, ws.slots, nseg, carry_key, carry);
+          if (lane == 0) flush_run<K>(sh_, ws, nseg, carry_key, carry);
         }
-        if ((closeB >> lane) & 1u) flush_run<K>(sh_, ws.slots, nseg, key, val);
+        if ((closeB >> lane) & 1u) flush_run<K>(sh_, ws, nseg, key, val);
         carry_key = __shfl_sync(0xFFFFFFFFu, key, lastl);
         carry = shfl_t(val, lastl);
         carry_valid = true;
@@ -441,79 +473,57 @@ __global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
           } else if (F.single) {
             A.lval = m;
           } else {
-            flush_run<K>(sh_, ws.slots, nseg, A.lkey, m);
+            flush_run<K>(sh_, ws, nseg, A.lkey, m);
             A.lkey = F.lkey;
             A.lval = F.lval;
           }
         } else {
-          if (!A.single) flush_run<K>(sh_, ws.slots, nseg, A.lkey, A.lval);
-          if (!F.single) flush_run<K>(sh_, ws.slots, nseg, F.fkey, F.fval);
+          if (!A.single) flush_run<K>(sh_, ws, nseg, A.lkey, A.lval);
+          if (!F.single) flush_run<K>(sh_, ws, nseg, F.fkey, F.fval);
           A.lkey = F.lkey;
           A.lval = F.lval;
           A.single = 0;
         }
       }
       if (A.has) {
-        flush_run<K>(sh_, ws.slots, nseg, A.fkey, A.fval);
-        if (!A.single) flush_run<K>(sh_, ws.slots, nseg, A.lkey, A.lval);
+        flush_run<K>(sh_, ws, nseg, A.fkey, A.fval);
+        if (!A.single) flush_run<K>(sh_, ws, nseg, A.lkey, A.lval);
       }
     }
     __syncthreads();
 
-    // ---- tile aggregate per stream, decoupled look-back
-    if (warp == 0) {
-      if (lane < K) {
-        StreamAgg a;
-        uint32_t ns = sh_.off[lane + 1] - sh_.off[lane];
-        a.n = ns;
-        a.fkey = sh_.fkey[lane];
-        a.lkey = sh_.lkey[lane];
-        a.single = (ns == 0) || (a.fkey == a.lkey);
-        a.lval = (ns == 0) ? rv_ident() : sh_.last_run[lane];
-        sh_.agg[lane] = a;
-      }
-      __syncwarp();
-      StreamAgg mine[K], pre[K];
+    // ---- stream offsets: count-only decoupled look-back (whole block)
+    if (tid < K) sh_.cnt[tid] = sh_.off[tid + 1] - sh_.off[tid];
+    __syncthreads();
+    if (tile > 0) {
+      if (tid == 0) lb_publish<K>(ws.lb_round, tile, tag16, LB_AGG, sh_.cnt);
+      lb_lookback<K>(ws.lb_round, tile, tag16, sh_.prefix, sh_.stop);
+    } else if (tid < K) {
+      sh_.prefix[tid] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
 #pragma unroll
-      for (int s = 0; s < K; s++) mine[s] = sh_.agg[s];
-      if (tile == 0) {
+      for (int s = 0; s < K; s++) sh_.incl[s] = sh_.prefix[s] + sh_.cnt[s];
+      lb_publish<K>(ws.lb_round, tile, tag16, LB_INC, sh_.incl);
+      // tile-boundary runs of children that may span tiles: merge into the
+      // block's pending run (children are contiguous, so consecutive tiles
+      // of a long child keep hitting the same pending run)
 #pragma unroll
-        for (int s = 0; s < K; s++) pre[s] = sa_identity();
-      } else {
-        lookback_publish_agg<StreamAgg, K, sa_identity, sa_combine>(ws.lb_flag_round, ws.lb_agg_round,
-                                                                    tile, tag, mine);
-        lookback_wait<StreamAgg, K, sa_identity, sa_combine>(ws.lb_flag_round, ws.lb_agg_round,
-                                                             ws.lb_incl_round, tile, tag,
-                                                             sh_.window, pre);
-      }
-      StreamAgg inc[K];
-#pragma unroll
-      for (int s = 0; s < K; s++) inc[s] = sa_combine(pre[s], mine[s]);
-      lookback_publish_incl<StreamAgg, K, sa_identity, sa_combine>(ws.lb_flag_round, ws.lb_incl_round,
-                                                                   tile, tag, inc);
-      if (lane < K) sh_.prefix[lane] = pre[lane];
-      // ---- close runs that this tile can now finalise
-      if (lane < K) {
-        StreamAgg P = pre[lane], A = mine[lane];
-        if (A.n > 0) {
-          if (P.n > 0 && P.lkey != A.fkey) st_cg(&ws.slots[P.lkey], P.lval);
-          RunVal firstv = (P.n > 0 && P.lkey == A.fkey) ? rv_merge(P.lval, sh_.first[lane])
-                                                         : sh_.first[lane];
-          if (!A.single) st_cg(&ws.slots[A.fkey], firstv);
-          if (last_tile) st_cg(&ws.slots[A.lkey], A.single ? firstv : sh_.last_run[lane]);
-        } else if (last_tile && P.n > 0) {
-          st_cg(&ws.slots[P.lkey], P.lval);
-        }
+      for (int s = 0; s < K; s++) {
+        if (sh_.cnt[s] == 0) continue;
+        pend_push(sh_, ws, s, sh_.fkey[s], sh_.first[s]);
+        if (sh_.lkey[s] != sh_.fkey[s]) pend_push(sh_, ws, s, sh_.lkey[s], sh_.last_run[s]);
       }
       // ---- finalise the launch
-      if (last_tile && lane == 0) {
+      if (last_tile) {
         uint32_t tot = 0;
         BookParams bp;
         bp.active = 1;
         bp.root = FIRST ? 1u : 0u;
         bp.nseg_parent = nseg;
-        for (int s = 0; s < 4; s++) bp.cnt_out[s] = (s < K) ? inc[s].n : 0u;
-        for (int s = 0; s < K; s++) tot += inc[s].n;
+        for (int s = 0; s < 4; s++) bp.cnt_out[s] = (s < K) ? sh_.incl[s] : 0u;
+        for (int s = 0; s < K; s++) tot += sh_.incl[s];
         bp.n_out = tot;
         bp.cur = cur;
         bp.h = FIRST ? st->h_final : st->rp.h;
@@ -538,13 +548,17 @@ __global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
     // ---- copy-out (coalesced per stream)
     for (uint32_t e = tid; e < N; e += BLOCK) {
       uint32_t s = (e >= sh_.off[1]) + (K == 3 ? (e >= sh_.off[2]) : 0);
-      size_t dst = (size_t)s * rcap + sh_.prefix[s].n + (e - sh_.off[s]);
+      size_t dst = (size_t)s * rcap + sh_.prefix[s] + (e - sh_.off[s]);
       outx[dst] = sx[e];
       outy[dst] = sy[e];
       if (DIM == 3) outz[dst] = sz[e];
       outi[dst] = sidx[e];
     }
     __syncthreads();
+  }
+  if (tid == 0) {
+    for (int s = 0; s < K; s++)
+      if (sh_.pend_valid[s]) flush_atomic(ws, sh_.pend_key[s], sh_.pend[s]);
   }
   if (FIRST && DIM == 3) {
     // coplanarity check input: max |d| of the first split (quickhull.py:349)
