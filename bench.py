@@ -1,0 +1,349 @@
+"""Benchmark of the B200 Quickhull hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A "step" is one whole hull of the configured workload: every Quickhull
+round of it, from the first bbox/extreme pass to the last vertex, as ONE
+CUDA-graph launch through the C ABI (the round loop runs on the device).
+
+Default workload (N=1): BASELINE.json configs[1] = C2, 2D Quickhull of 100M
+points uniform in the unit disk (fp64, reference generator, seed 0).  The
+other configs are parity cases (tests/), selectable here with --config.
+
+value     Mpoints/s = n * K / (device time of K hulls), input resident in HBM
+          (1.6 GB, far larger than the 126 MB L2, so no flush is needed).
+e2e       same metric through the public API with HOST (pinned) buffers:
+          H2D copy of the points + hull + D2H of the vertex indices per step.
+roofline  the fused round kernel (k_round): algorithmic bytes of each launch
+          (R_d*(n_r + n_{r+1}), first split 8*dim*n +
+          R_d*n_1, R_d = 8*dim + 4) over its CUDA-event duration, measured in
+          an event-instrumented pass (launch mode 2) right after the timed
+          region; peak = MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the oracle (single-threaded C restatement of the reference
+          drivers) on the same workload, rank 0, N=1 only.
+
+--impl reference: the reference's CPU implementation of the path -- here the
+oracle port, since the reference is pure Python and cannot travel to the GPU
+box -- timed on a bounded sample of the same workload (the first 10M points of
+the same cloud), rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpoints/sec for 2D/3D hull (device-timed) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "Mpoints/s"
+
+CONFIGS = {
+    "C1": ("C1: 2D Quickhull, 1M points uniform in unit square (fp64)", "unit-square", 1_000_000),
+    "C2": ("C2: 2D Quickhull, 100M points uniform in unit disk (fp64)", "uniform-disk", 100_000_000),
+    "C3": ("C3: 2D Quickhull, 10M points on unit circle (fp64)", "on-circle", 10_000_000),
+    "C3n": ("C3': 2D Quickhull, 10M points near unit circle, band 0.01 (fp64)", "near-circle",
+            10_000_000),
+    "C4c": ("C4: 3D Quickhull, 10M points uniform in unit cube (fp64)", "unit-cube", 10_000_000),
+    "C4b": ("C4: 3D Quickhull, 10M points uniform in unit ball (fp64)", "uniform-ball", 10_000_000),
+}
+REF_SAMPLE = 10_000_000
+
+KID_ROUND_FIRST, KID_ROUND = 3, 4
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        self.t.join(timeout=2)
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in self.rows if num(r[0])]
+        mx = [num(r[1]) for r in self.rows if num(r[1])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(cfg):
+    """ncu dram bytes per k_round launch from the committed full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "round_traffic.json")) as f:
+            return json.load(f).get(cfg)
+    except (OSError, ValueError):
+        return None
+
+
+def gen(kind, n):
+    from paper_1201_2936_b200.datagen import generate
+    return generate(kind, n, 0)
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import oracle
+    desc, kind, n = CONFIGS[args.config]
+    m = min(n, REF_SAMPLE)
+    cols = gen(kind, m)
+    fn = oracle.hull2d if len(cols) == 2 else oracle.hull3d
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = fn(*cols)
+        dt = time.perf_counter() - t0
+        assert r.status == 0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = m * len(times) / tot / 1e6
+    sample = (f"first {m:,} points of the {args.config} cloud (same generator/seed) per step; "
+              f"single-threaded C restatement of the reference drivers (oracle/qh_oracle.c)")
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * tot / len(times), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "n": m, "sample_of": n},
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import ctypes
+
+    import paper_1201_2936_b200 as P
+    from paper_1201_2936_b200 import _lib
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    desc, kind, n = CONFIGS[args.config]
+    cols = gen(kind, n)
+    dim = len(cols)
+    host = tuple(torch.from_numpy(c).pin_memory() for c in cols)
+    d = tuple(h.to("cuda", non_blocking=True) for h in host)
+    torch.cuda.synchronize()
+    L, ctx = _lib.lib(), _lib.context(local)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    fac = None
+    res = _lib.ShResult()
+    ptrs = [t.data_ptr() for t in d]
+    nan = float("nan")
+
+    def launch():
+        if dim == 2:
+            rc = L.sh_hull2d_async(ctx, ptrs[0], ptrs[1], 1, n, 1e-12, nan, out.data_ptr(), sp)
+        else:
+            rc = L.sh_hull3d_async(ctx, ptrs[0], ptrs[1], ptrs[2], 1, n, 1e-12, nan, out.data_ptr(),
+                                   None, 0, sp)
+        if rc:
+            raise RuntimeError(_lib.last_error())
+
+    # sync API once: sizes the segment tables (overflow retries happen here)
+    f = P.hull_indices_2d if dim == 2 else P.hull_indices_3d
+    f(d)
+    for _ in range(args.warmup):
+        launch()
+    torch.cuda.synchronize()
+    assert L.sh_fetch(ctx, ctypes.byref(res), sp) == 0
+    rounds, h = int(res.iterations), int(res.h)
+
+    # ---------------- timed region: K whole hulls, device-timed
+    clk = Clocks(local)
+    clk.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for i in range(args.steps):
+        launch()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    tot_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    assert L.sh_fetch(ctx, ctypes.byref(res), sp) == 0
+    assert int(res.h) == h and int(res.iterations) == rounds
+    value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
+    launches_per_hull = 5 + 2 * rounds + (2 if dim == 3 else 0)
+
+    # ---------------- per-kernel pass (events after every launch)
+    tr = P.trace(local)
+    L.sh_set_launch_mode(ctx, 2)
+    per = []
+    for _ in range(3):
+        launch()
+        torch.cuda.synchronize()
+        kinds = np.zeros(4096, np.int32)
+        ms = np.zeros(4096, np.float32)
+        k = L.sh_launch_times(ctx, kinds.ctypes.data, ms.ctypes.data, 4096)
+        per.append((kinds[:k].copy(), ms[:k].copy()))
+    L.sh_set_launch_mode(ctx, 0)
+    Rd = 8 * dim + 4
+    n1 = int(tr[0, 0]) if len(tr) else 0
+    round_bytes = [8 * dim * n + Rd * n1] + [Rd * (int(a) + int(b)) for a, b, _, _ in tr]
+    best = None
+    for kinds, ms in per:
+        rt = ms[(kinds == KID_ROUND_FIRST) | (kinds == KID_ROUND)]
+        if len(rt) != len(round_bytes):
+            continue
+        tot_round = float(rt.sum())
+        if best is None or tot_round < best[0]:
+            best = (tot_round, float(ms.sum()), rt)
+    peak, peak_src = measured_peak()
+    roofline = None
+    if best:
+        tot_round, tot_all, rt = best
+        launches = len(round_bytes)
+        achieved = sum(round_bytes) / launches / (tot_round / launches / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_round (fused round: discard+classify+regroup+argmax)",
+                    "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": committed_traffic(args.config),
+                    "peak_source": peak_src, "launches": launches,
+                    "algorithmic_bytes_per_launch": int(sum(round_bytes) / launches),
+                    "avg_launch_ms": round(tot_round / launches, 4),
+                    "share_of_kernel_time": round(tot_round / tot_all, 3),
+                    "whole_hull_frac": round(
+                        (sum(round_bytes) + 8 * dim * n) / (tot_ms / args.steps / 1e3) / 1e9 / peak, 4),
+                    "per_round_gbs": [round(b / (t / 1e3) / 1e9, 1) for b, t in zip(round_bytes, rt)]}
+
+    # ---------------- e2e: public API, pinned host buffers in, indices out
+    e2e_ms = []
+    for i in range(min(args.steps, 5) + 1):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        idx_host = f(host)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            e2e_ms.append(e0.elapsed_time(e1))
+    e2e_val = n * ws / (statistics.mean(e2e_ms) / 1e3) / 1e6
+    assert idx_host.numel() == h
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        fn = oracle.hull2d if dim == 2 else oracle.hull3d
+        t0 = time.perf_counter()
+        r = fn(*cols)
+        dt = time.perf_counter() - t0
+        assert r.status == 0 and len(r.idx) == res.candidates
+        cpu = {"value": round(n / dt / 1e6, 3), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"the whole {args.config} workload ({n:,} points), one run, "
+                         "single-threaded C restatement of the reference drivers (oracle/)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "n": n, "dim": dim, "rounds": rounds, "hull": h,
+                           "candidates": int(res.candidates), "eps_rel": 1e-12,
+                           "l2": "inputs (%.1f GB) larger than the 126 MB L2; no flush" %
+                                 (8 * dim * n / 1e9),
+                           "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+                "e2e": {"value": round(e2e_val, 2), "unit": UNIT,
+                        "h2d_bytes_per_step": 8 * dim * n, "d2h_bytes_per_step": 8 * h,
+                        "ms_per_step": round(statistics.mean(e2e_ms), 3)},
+                "gpu_launches": launches_per_hull * args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

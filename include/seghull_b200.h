@@ -100,8 +100,15 @@ void sh_hypot_host(const double* x, const double* y, double* out, int64_t n);
 
 /* 0 (default): one CUDA-graph launch per hull, round loop on the device.
  * 1: host-driven round loop (one sync per round) -- for profilers that can
- * not attribute kernels inside conditional graphs. */
+ * not attribute kernels inside conditional graphs.
+ * 2: as 1, plus a CUDA event after every kernel launch (sh_launch_times). */
 int sh_set_launch_mode(sh_ctx* ctx, int mode);
+
+/* Kernel launches of the last hull run in launch mode 2, in launch order:
+ * kernel id (0 init, 1 first reduce, 2 line-far, 3 first-split round,
+ * 4 round, 5 bookkeeping, 6 3D filter, 7 output) and device time in ms
+ * (event to event on the hull's stream).  Returns the count written. */
+int64_t sh_launch_times(sh_ctx* ctx, int32_t* kind, float* ms, int64_t cap);
 
 const char* sh_last_error(void);
 const char* sh_version(void);

@@ -52,8 +52,27 @@ struct sh_ctx {
   Graph g[4];
   int round_occ = 0, book_occ = 0;
   uint32_t last_n = 0;
-  int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop (profiling)
+  int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
+  // per-launch CUDA events (launch_mode 2): ev[0] before the first launch,
+  // ev[i+1] after launch i, whose kernel is prof_kind[i]
+  static constexpr int PROF_CAP = 8192;
+  cudaEvent_t ev[PROF_CAP + 1] = {};
+  int prof_kind[PROF_CAP] = {};
+  int prof_n = 0;
+  bool prof_on = false;
 };
+
+// Kernel ids reported by sh_launch_times (include/seghull_b200.h).
+enum { KID_INIT = 0, KID_FIRST_REDUCE, KID_LINE_FAR, KID_ROUND_FIRST, KID_ROUND, KID_BOOK,
+       KID_FILTER, KID_OUTPUT };
+
+static void prof_mark(sh_ctx* c, cudaStream_t s, int kind) {
+  if (!c->prof_on || c->prof_n >= sh_ctx::PROF_CAP) return;
+  if (!c->ev[c->prof_n + 1]) cudaEventCreate(&c->ev[c->prof_n + 1]);
+  c->prof_kind[c->prof_n] = kind;
+  cudaEventRecord(c->ev[c->prof_n + 1], s);
+  c->prof_n++;
+}
 
 #define CK(x)                                                                     \
   do {                                                                            \
@@ -175,8 +194,10 @@ static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
   k_round<DIM, false><<<ws.round_grid, BLOCK, dsm, s>>>(ws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_ROUND);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_BOOK);
   return SH_OK;
 }
 
@@ -185,16 +206,21 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
   k_init<DIM><<<1, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_INIT);
   k_first_reduce<DIM><<<ws.red_blocks, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_FIRST_REDUCE);
   if (DIM == 3) {
     k_line_far<<<ws.red_blocks, BLOCK, 0, s>>>(ws);
     CK(cudaGetLastError());
+    prof_mark(c, s, KID_LINE_FAR);
   }
   k_round<DIM, true><<<ws.round_grid, BLOCK, dsm, s>>>(ws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_ROUND_FIRST);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_BOOK);
   return SH_OK;
 }
 
@@ -203,9 +229,11 @@ static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
   if (DIM == 3) {
     int rc = filter_launch(c->fws, ws, c->nsm, s);
     if (rc) return rc;
+    prof_mark(c, s, KID_FILTER);
   }
   k_output<DIM><<<c->nsm * 4, BLOCK, 0, s>>>(ws, c->fws);
   CK(cudaGetLastError());
+  prof_mark(c, s, KID_OUTPUT);
   return SH_OK;
 }
 
@@ -301,6 +329,12 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     // attribute kernels inside graphs that contain conditional nodes)
     Workspace ws = c->ws;
     ws.use_cond = 0;
+    c->prof_on = (c->launch_mode == 2);
+    c->prof_n = 0;
+    if (c->prof_on) {
+      if (!c->ev[0]) cudaEventCreate(&c->ev[0]);
+      cudaEventRecord(c->ev[0], s);
+    }
     rc = launch_pre<DIM>(c, ws, s);
     if (rc) return rc;
     for (;;) {
@@ -311,6 +345,7 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
       if (rc) return rc;
     }
     rc = launch_post<DIM>(c, ws, s);
+    c->prof_on = false;
     if (rc) return rc;
   }
   c->last_n = (uint32_t)n;
@@ -408,6 +443,8 @@ void sh_destroy(sh_ctx* c) {
   cudaSetDevice(c->device);
   free_ws(c);
   if (c->st_host) cudaFreeHost(c->st_host);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
   if (c->build_stream) cudaStreamDestroy(c->build_stream);
   if (c->body_stream) cudaStreamDestroy(c->body_stream);
   delete c;
@@ -479,9 +516,24 @@ void sh_hypot_host(const double* x, const double* y, double* out, int64_t n) {
 }
 
 int sh_set_launch_mode(sh_ctx* c, int mode) {
-  if (!c || (mode != 0 && mode != 1)) return set_err(SH_CONTRACT, "mode must be 0 (graph) or 1 (host loop)");
+  if (!c || mode < 0 || mode > 2)
+    return set_err(SH_CONTRACT, "mode must be 0 (graph), 1 (host loop) or 2 (host loop + events)");
   c->launch_mode = mode;
   return SH_OK;
+}
+
+int64_t sh_launch_times(sh_ctx* c, int32_t* kind, float* ms, int64_t cap) {
+  if (!c) return 0;
+  if (cudaSetDevice(c->device) != cudaSuccess) return 0;
+  int64_t n = std::min<int64_t>(c->prof_n, cap);
+  for (int64_t i = 0; i < n; i++) {
+    if (cudaEventSynchronize(c->ev[i + 1]) != cudaSuccess) return i;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]);
+    if (kind) kind[i] = c->prof_kind[i];
+    if (ms) ms[i] = t;
+  }
+  return n;
 }
 
 const char* sh_last_error(void) { return g_last_error.c_str(); }

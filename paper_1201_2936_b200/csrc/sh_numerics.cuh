@@ -63,7 +63,7 @@ SH_HD double hypot_kernel(double ax, double ay) {
 SH_HD double glibc_hypot(double x, double y) {
   const double SCALE = 0x1p-600;
   const double LARGE_VAL = 0x1p+511;
-  const double TINY_VAL = 0x1p-511;
+  const double TINY_VAL = 0x1p-459;  // keeps the kernel's squares and deltas normal
   const double EPS = 0x1p-54;
   if (!isfinite(x) || !isfinite(y)) {
     if (isinf(x) || isinf(y)) return INFINITY;

@@ -60,6 +60,20 @@ def _raise_for(rc: int):
     raise RuntimeError(f"seghull_b200 error {rc}: {msg}")
 
 
+def _on_host(points):
+    first = points[0] if isinstance(points, (tuple, list)) else points
+    return torch.is_tensor(first) and first.device.type == "cpu"
+
+
+def _to_cuda(points):
+    """Host tensors (ideally pinned) -> the current CUDA device, async on the
+    current stream; the hull launch that follows is ordered after the copy."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if isinstance(points, (tuple, list)):
+        return tuple(c.to(dev, non_blocking=True) for c in points)
+    return points.to(dev, non_blocking=True)
+
+
 def _as_device_coords(points, dim):
     """(n, dim) fp64 CUDA tensor (any row stride with unit column stride) or
     a tuple of dim 1-D fp64 CUDA tensors -> (pointers, stride, n, keepalive)."""
@@ -92,7 +106,15 @@ def _stream_ptr(device):
 
 
 def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False):
-    """Original indices (int64 CUDA tensor) of the 2D hull vertices."""
+    """Original indices (int64 tensor) of the 2D hull vertices.
+
+    ``points``: an (n, 2) float64 tensor or a pair of 1-D float64 tensors.
+    CUDA input -> CUDA output, no host synchronisation beyond reading the
+    vertex count.  Host (CPU, preferably pinned) input is copied to the
+    current device first and the indices come back on the host."""
+    if _on_host(points):
+        r = hull_indices_2d(_to_cuda(points), tol, return_info)
+        return (r[0].cpu(), r[1]) if return_info else r.cpu()
     ptrs, stride, n, keep = _as_device_coords(points, 2)
     device = keep[0].device.index
     if n == 0:
@@ -109,8 +131,14 @@ def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False):
 
 
 def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False):
-    """Original indices (int64 CUDA tensor) of the 3D hull vertices, plus the
-    (f, 3) int32 facet triples when ``facets`` is true."""
+    """Original indices (int64 tensor) of the 3D hull vertices, plus the
+    (f, 3) int32 facet triples when ``facets`` is true.  Host input is
+    handled like in hull_indices_2d."""
+    if _on_host(points):
+        r = hull_indices_3d(_to_cuda(points), tol, facets, return_info)
+        if return_info:
+            return r[0].cpu(), (None if r[1] is None else r[1].cpu()), r[2]
+        return (r[0].cpu(), None if r[1] is None else r[1].cpu()) if facets else r.cpu()
     ptrs, stride, n, keep = _as_device_coords(points, 3)
     device = keep[0].device.index
     if n == 0:

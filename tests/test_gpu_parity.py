@@ -1,0 +1,206 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and against the oracle (the C restatement of the reference
+drivers, itself pinned by test_oracle.py) on seeded inputs up to the full
+benchmark sizes.  Bar: bit-exact vertex index sets, identical iteration
+counts, per-round traces and warning strings."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1201_2936_b200 as P
+from golden_io import load, rows_of
+from paper_1201_2936_b200.datagen import generate
+
+pytestmark = pytest.mark.gpu
+
+CASES = load()
+C2 = [c for c in CASES if c.dim == 2]
+C3 = [c for c in CASES if c.dim == 3]
+
+
+def dev(cols):
+    return tuple(torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in cols)
+
+
+def vset(rows):
+    return set(map(tuple, np.asarray(rows).tolist()))
+
+
+@pytest.mark.parametrize("case", C2, ids=[c.name for c in C2])
+def test_golden_2d(case):
+    r = P.quickhull_2d(P.PointSet(case.coords))
+    assert vset(r.vertices.as_rows()) == vset(case.verts)
+    assert r.vertices.n == case.h
+    assert r.iterations == case.iterations
+    assert r.discarded == case.discarded
+    assert r.warnings == case.warnings
+    assert P.trace()[:, :3].tolist() == case.trace
+
+
+@pytest.mark.parametrize("case", C3, ids=[c.name for c in C3])
+def test_golden_3d(case):
+    if case.error:
+        with pytest.raises(getattr(P, case.error)):
+            P.quickhull_3d(P.PointSet(case.coords))
+        return
+    r = P.quickhull_3d(P.PointSet(case.coords))
+    assert r.iterations == case.iterations
+    assert P.trace()[:, :3].tolist() == case.trace
+    assert vset(r.vertices.as_rows()) == vset(case.verts)
+    assert r.discarded == case.discarded
+    assert r.warnings == case.warnings
+
+
+def _check2(cols, eps_rel=1e-12):
+    o = oracle.hull2d(*cols, eps_rel=eps_rel)
+    idx, res = P.hull_indices_2d(dev(cols), P.Tolerance(eps_rel), return_info=True)
+    got = np.sort(idx.cpu().numpy())
+    assert np.array_equal(got, np.sort(o.idx))
+    assert res.iterations == o.iterations
+    assert np.array_equal(P.trace()[:, :3], o.trace)
+    return got, res
+
+
+def _check3(cols, eps_rel=1e-12):
+    o, idx_ref, warns = oracle.full_hull3d(*cols, eps_rel=eps_rel)
+    idx, _, res = P.hull_indices_3d(dev(cols), P.Tolerance(eps_rel), return_info=True)
+    assert res.iterations == o.iterations
+    tr = P.trace()
+    assert np.array_equal(tr[:, :3], o.trace)
+    assert np.array_equal(tr[:, 3], o.flat_counts[:len(tr)])
+    assert res.candidates == len(o.idx)
+    assert np.array_equal(np.sort(idx.cpu().numpy()), np.sort(idx_ref))
+    return res
+
+
+@pytest.mark.parametrize("kind", ["unit-square", "uniform-disk", "on-circle", "near-circle"])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 64, 2049, 100_000, 1_000_000])
+def test_random_2d_vs_oracle(kind, n):
+    for seed in range(2):
+        _check2(generate(kind, n, seed))
+
+
+@pytest.mark.parametrize("kind", ["unit-cube", "uniform-ball", "on-sphere", "near-sphere"])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 64, 2049, 100_000, 1_000_000])
+def test_random_3d_vs_oracle(kind, n):
+    for seed in range(2):
+        _check3(generate(kind, n, seed))
+
+
+def test_eps_variants_2d():
+    cols = generate("near-circle", 200_000, 3)
+    for e in (0.0, 1e-15, 1e-9, 1e-6):
+        _check2(cols, e)
+
+
+def test_strided_rows_and_host_input():
+    x, y = generate("uniform-disk", 300_000, 2)
+    rows = torch.from_numpy(np.column_stack([x, y]))
+    a = np.sort(P.hull_indices_2d(rows.cuda()).cpu().numpy())
+    b = np.sort(P.hull_indices_2d((torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())).cpu().numpy())
+    c = np.sort(P.hull_indices_2d(rows.pin_memory()).numpy())
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    # column view of a wider row-major array (stride 3)
+    wide = torch.from_numpy(np.column_stack([x, y, np.zeros_like(x)])).cuda()
+    d = np.sort(P.hull_indices_2d(wide[:, :2]).cpu().numpy())
+    assert np.array_equal(a, d)
+
+
+def test_idempotent_and_permutation_invariant():
+    x, y = generate("near-circle", 400_000, 5)
+    base, _ = _check2((x, y))
+    again = np.sort(P.hull_indices_2d(dev((x[base], y[base]))).cpu().numpy())
+    assert np.array_equal(base[again], base)  # every vertex is a vertex of the vertex hull
+    perm = np.random.default_rng(0).permutation(x.size)
+    p = P.hull_indices_2d(dev((x[perm], y[perm]))).cpu().numpy()
+    assert np.array_equal(np.sort(perm[p]), base)
+
+
+def test_repeat_calls_and_workspace_regrowth():
+    big = generate("uniform-disk", 2_000_000, 0)
+    small = generate("unit-square", 1000, 0)
+    a = _check2(big)[0]
+    _check2(small)
+    b = _check2(big)[0]
+    assert np.array_equal(a, b)
+    _check3(generate("uniform-ball", 50_000, 0))
+    _check2(small)
+
+
+def test_many_segments_regrowth():
+    # on-circle: 500k+ segments per round forces segment-table regrowth
+    _check2(generate("on-circle", 3_000_000, 1))
+
+
+def test_degenerate_and_errors():
+    with pytest.raises(P.EmptyInputError):
+        P.hull_indices_2d(torch.empty((0, 2), dtype=torch.float64, device="cuda"))
+    with pytest.raises(P.ContractViolation):
+        P.hull_indices_2d(torch.zeros((5, 3), dtype=torch.float64, device="cuda"))
+    with pytest.raises(P.ContractViolation):
+        P.hull_indices_2d(torch.zeros((5, 2), dtype=torch.float32, device="cuda"))
+    with pytest.raises(P.DegenerateInputError):
+        xs = torch.rand(1000, dtype=torch.float64)
+        P.hull_indices_3d((xs.cuda(), torch.rand(1000, dtype=torch.float64).cuda(),
+                           torch.full((1000,), 0.25, dtype=torch.float64).cuda()))
+    line = P.quickhull_2d(P.PointSet.from_rows([(i, 2 * i) for i in range(1000)]))
+    assert vset(line.vertices.as_rows()) == {(0.0, 0.0), (999.0, 1998.0)}
+    assert line.warnings == ["collinear input: hull is the two x-extrema"]
+
+
+def test_async_api_matches_sync():
+    import ctypes
+    from paper_1201_2936_b200 import _lib
+    x, y = dev(generate("uniform-disk", 500_000, 9))
+    ref = np.sort(P.hull_indices_2d((x, y)).cpu().numpy())
+    out = torch.empty(x.numel(), dtype=torch.int64, device="cuda")
+    L, ctx = _lib.lib(), _lib.context(0)
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.sh_hull2d_async(ctx, x.data_ptr(), y.data_ptr(), 1, x.numel(), 1e-12,
+                             float("nan"), out.data_ptr(), s) == 0
+    res = _lib.ShResult()
+    assert L.sh_fetch(ctx, ctypes.byref(res), s) == 0
+    assert np.array_equal(np.sort(out[:res.h].cpu().numpy()), ref)
+
+
+def test_launch_times_hostloop_mode():
+    import ctypes
+    from paper_1201_2936_b200 import _lib
+    L, ctx = _lib.lib(), _lib.context(0)
+    cols = generate("uniform-disk", 1_000_000, 0)
+    L.sh_set_launch_mode(ctx, 2)
+    try:
+        got, res = _check2(cols)
+    finally:
+        L.sh_set_launch_mode(ctx, 0)
+    kind = np.zeros(256, np.int32)
+    ms = np.zeros(256, np.float32)
+    k = L.sh_launch_times(ctx, kind.ctypes.data, ms.ctypes.data, 256)
+    assert k == 4 + 2 * res.iterations + 1
+    assert (kind[:k] == 4).sum() == res.iterations
+    assert (ms[:k] > 0).all()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3n", "C4c", "C4b"])
+def test_full_size_configs(cfg):
+    """BASELINE.json configs 1-4 at full size, bit-exact against the oracle."""
+    if cfg == "C1":
+        _check2(generate("unit-square", 1_000_000, 0))
+    elif cfg == "C2":
+        got, res = _check2(generate("uniform-disk", 100_000_000, 0))
+        assert res.iterations == 12 and got.size == 1591
+    elif cfg == "C3":
+        got, res = _check2(generate("on-circle", 10_000_000, 0))
+        assert res.iterations == 21 and got.size == 2_071_874
+    elif cfg == "C3n":
+        got, res = _check2(generate("near-circle", 10_000_000, 0))
+        assert res.iterations == 13 and got.size == 2691
+    elif cfg == "C4c":
+        res = _check3(generate("unit-cube", 10_000_000, 0))
+        assert res.iterations == 12 and res.candidates == 1790 and res.h == 424
+    else:
+        res = _check3(generate("uniform-ball", 10_000_000, 0))
+        assert res.iterations == 15 and res.candidates == 34_625 and res.h == 14_152
