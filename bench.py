@@ -281,6 +281,10 @@ def main():
         tot_round = float(rt.sum())
         if best is None or tot_round < best[0]:
             best = (tot_round, float(ms.sum()), rt)
+            names = ["init", "first_reduce", "line_far", "round_first", "round", "book", "filter",
+                     "output"]
+            kernel_ms_by_kind = {names[k]: round(float(ms[kinds == k].sum()), 4)
+                                 for k in sorted(set(kinds.tolist()))}
     peak, peak_src = measured_peak()
     roofline = None
     if best:
@@ -296,7 +300,9 @@ def main():
                     "share_of_kernel_time": round(tot_round / tot_all, 3),
                     "whole_hull_frac": round(
                         (sum(round_bytes) + 8 * dim * n) / (tot_ms / args.steps / 1e3) / 1e9 / peak, 4),
-                    "per_round_gbs": [round(b / (t / 1e3) / 1e9, 1) for b, t in zip(round_bytes, rt)]}
+                    "per_round_gbs": [round(float(b / (t / 1e3) / 1e9), 1) for b, t in
+                                      zip(round_bytes, rt)],
+                    "kernel_ms_by_kind": kernel_ms_by_kind}
 
     # ---------------- e2e: public API, pinned host buffers in, indices out
     e2e_ms = []
