@@ -45,6 +45,7 @@ struct sh_ctx {
   int dim = 0;           // dim the workspace was sized for (2 or 3), 0 = none
   uint64_t cap_n = 0;    // points
   uint32_t segcap = 0;   // segments
+  uint32_t mcap = 0;     // 3D filter: candidates
   Workspace ws{};
   FilterWs fws{};
   size_t red_bytes = 0;
@@ -126,7 +127,7 @@ static void free_ws(sh_ctx* c) {
   c->segcap = 0;
 }
 
-static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap) {
+static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mcap) {
   free_ws(c);
   Workspace& w = c->ws;
   const int K = dim;
@@ -155,7 +156,7 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap) {
   w.red_blocks = (uint32_t)c->nsm * 8;
   ok &= cudaMalloc((void**)&w.red, (size_t)w.red_blocks * 128 + 256) == cudaSuccess;
   ok &= dalloc(&w.st, 1) == cudaSuccess;
-  if (ok && dim == 3) ok &= filter_alloc(c->fws, n) == 0;
+  if (ok && dim == 3) ok &= filter_alloc(c->fws, mcap) == 0;
   if (!ok) {
     free_ws(c);
     cudaGetLastError();
@@ -172,6 +173,7 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap) {
   c->dim = dim;
   c->cap_n = n;
   c->segcap = segcap;
+  c->mcap = (dim == 3) ? mcap : 0;
   return SH_OK;
 }
 
@@ -181,11 +183,19 @@ static uint32_t default_segcap(int dim, uint64_t n) {
   return (uint32_t)s;
 }
 
-static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min) {
+static uint32_t default_mcap(uint64_t n) {
+  uint64_t m = std::max<uint64_t>(1u << 16, n / 64);
+  return (uint32_t)std::min<uint64_t>(m, n + 4);
+}
+
+static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min, uint32_t mcap_min) {
   uint32_t want = std::max(default_segcap(dim, n), segcap_min);
-  if (c->dim == dim && c->cap_n >= n && c->segcap >= want) return SH_OK;
-  uint64_t cap = std::max<uint64_t>(n, (c->dim == dim) ? c->cap_n : 0);
-  return alloc_ws(c, dim, cap, std::max(want, (c->dim == dim) ? c->segcap : 0u));
+  uint32_t mwant = (dim == 3) ? std::max(default_mcap(n), mcap_min) : 0u;
+  if (c->dim == dim && c->cap_n >= n && c->segcap >= want && c->mcap >= mwant) return SH_OK;
+  bool same = c->dim == dim;
+  uint64_t cap = std::max<uint64_t>(n, same ? c->cap_n : 0);
+  return alloc_ws(c, dim, cap, std::max(want, same ? c->segcap : 0u),
+                  std::max(mwant, same ? c->mcap : 0u));
 }
 
 // ---------------------------------------------------------------- graph
@@ -230,6 +240,7 @@ static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
     int rc = filter_launch(c->fws, ws, c->nsm, s);
     if (rc) return rc;
     prof_mark(c, s, KID_FILTER);
+    return SH_OK;
   }
   k_output<DIM><<<c->nsm * 4, BLOCK, 0, s>>>(ws, c->fws);
   CK(cudaGetLastError());
@@ -291,14 +302,14 @@ static int build_graph(sh_ctx* c) {
 template <int DIM>
 static int hull_async(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
                       int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* facets,
-                      int64_t facet_cap, cudaStream_t s, uint32_t segcap_min) {
+                      int64_t facet_cap, cudaStream_t s, uint32_t segcap_min, uint32_t mcap_min) {
   if (n <= 0) return set_err(SH_EMPTY, "cannot take the hull of an empty point set");
   if (n >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "n must be < 2^31");
   if (!x || !y || (DIM == 3 && !z) || !out_idx) return set_err(SH_CONTRACT, "null pointer");
   if (stride < 1) return set_err(SH_CONTRACT, "stride must be >= 1");
   if (!(eps_rel >= 0)) return set_err(SH_CONTRACT, "eps_rel must be nonnegative");
   CK(cudaSetDevice(c->device));
-  int rc = ensure_ws(c, DIM, (uint64_t)n, segcap_min);
+  int rc = ensure_ws(c, DIM, (uint64_t)n, segcap_min, mcap_min);
   if (rc) return rc;
   rc = build_graph<DIM>(c);
   if (rc) return rc;
@@ -372,7 +383,7 @@ static int fetch(sh_ctx* c, sh_result* res, cudaStream_t s) {
       res->facets = (int64_t)fres[1];
     }
   }
-  if (h->status == ST_SEG_OVERFLOW) return SH_OK;  // caller retries
+  if (h->status == ST_SEG_OVERFLOW || h->status == ST_CAND_OVERFLOW) return SH_OK;  // caller retries
   if (h->status == ST_DEGENERATE)
     return set_err(SH_DEGENERATE, "all points are coplanar; project to the plane and use the 2D driver");
   if (h->status == ST_ROUND_GUARD) return set_err(SH_ROUND_GUARD, "round count exceeded the input size");
@@ -383,15 +394,17 @@ template <int DIM>
 static int hull_sync(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
                      int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* facets,
                      int64_t facet_cap, sh_result* res, cudaStream_t s) {
-  uint32_t segmin = 0;
+  uint32_t segmin = 0, mmin = 0;
   for (int attempt = 0; attempt < 8; attempt++) {
     int rc = hull_async<DIM>(c, x, y, z, stride, n, eps_rel, eps_abs, out_idx, facets, facet_cap, s,
-                             segmin);
+                             segmin, mmin);
     if (rc) return rc;
     rc = fetch(c, res, s);
-    if (c->st_host->status != ST_SEG_OVERFLOW) return rc;
+    const uint32_t stt = c->st_host->status;
+    if (stt != ST_SEG_OVERFLOW && stt != ST_CAND_OVERFLOW) return rc;
     uint64_t need = (uint64_t)c->st_host->seg_needed * 2 + 1024;
-    segmin = (uint32_t)std::min<uint64_t>(need, (uint64_t)n + 4);
+    if (stt == ST_SEG_OVERFLOW) segmin = (uint32_t)std::min<uint64_t>(need, (uint64_t)n + 4);
+    else mmin = (uint32_t)std::min<uint64_t>(need, (uint64_t)n + 4);
   }
   return set_err(SH_NOMEM, "segment table capacity retries exhausted");
 }
@@ -453,7 +466,7 @@ void sh_destroy(sh_ctx* c) {
 int sh_reserve(sh_ctx* c, int dim, int64_t n) {
   if (!c || (dim != 2 && dim != 3) || n <= 0) return set_err(SH_CONTRACT, "bad reserve arguments");
   CK(cudaSetDevice(c->device));
-  int rc = ensure_ws(c, dim, (uint64_t)n, 0);
+  int rc = ensure_ws(c, dim, (uint64_t)n, 0, 0);
   if (rc) return rc;
   return dim == 2 ? build_graph<2>(c) : build_graph<3>(c);
 }
@@ -477,7 +490,7 @@ int sh_hull2d_async(sh_ctx* c, const double* x, const double* y, int64_t stride,
                     double eps_rel, double eps_abs, int64_t* out_idx, void* stream) {
   if (!c) return set_err(SH_CONTRACT, "null context");
   return hull_async<2>(c, x, y, nullptr, stride, n, eps_rel, eps_abs, out_idx, nullptr, 0,
-                       (cudaStream_t)stream, 0);
+                       (cudaStream_t)stream, 0, 0);
 }
 
 int sh_hull3d_async(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
@@ -485,14 +498,14 @@ int sh_hull3d_async(sh_ctx* c, const double* x, const double* y, const double* z
                     int64_t facet_cap, void* stream) {
   if (!c) return set_err(SH_CONTRACT, "null context");
   return hull_async<3>(c, x, y, z, stride, n, eps_rel, eps_abs, out_idx, out_facets, facet_cap,
-                       (cudaStream_t)stream, 0);
+                       (cudaStream_t)stream, 0, 0);
 }
 
 int sh_fetch(sh_ctx* c, sh_result* res, void* stream) {
   if (!c) return set_err(SH_CONTRACT, "null context");
   int rc = fetch(c, res, (cudaStream_t)stream);
-  if (c->st_host->status == ST_SEG_OVERFLOW)
-    return set_err(SH_NOMEM, "segment table overflow; use the synchronous call (it retries)");
+  if (c->st_host->status == ST_SEG_OVERFLOW || c->st_host->status == ST_CAND_OVERFLOW)
+    return set_err(SH_NOMEM, "segment/candidate table overflow; use the synchronous call (it retries)");
   return rc;
 }
 
