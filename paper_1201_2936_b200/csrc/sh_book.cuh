@@ -1,12 +1,15 @@
 // K3: per-segment bookkeeping between rounds.
 //
-// Input: the child results written by the round kernel into `slots`
-// (stream-order child id e = s*nseg_parent + parent: farthest key, lowest
-// index, count).  One persistent launch, one thread per child:
+// Input: the child results of the round kernel (child id e = parent*K +
+// state: farthest key in slot_key, survivor count = write cursor - parent
+// start).  One persistent launch, one thread per child:
 //   * occupied children (count > 0) get dense ids by a decoupled look-back
-//     scan over (occupied, count, emitted) -- the dense order is the stream
-//     order, which is exactly the order the round kernel wrote the
-//     survivors in, so the scanned counts are the segments' start positions;
+//     scan over (occupied, count, emitted) in parent-major order -- the
+//     reference's flat-array segment order -- which also gives every new
+//     segment its dense start and every emitted vertex its output position;
+//   * the new segment's records stay where the round kernel wrote them:
+//     stream s at the parent's start (seg_phys), and its children's write
+//     cursors are initialised to its own dense start;
 //   * child tables are built once per segment (2D: the child edge and the
 //     three glibc-exact hypot thresholds, quickhull.py:268-277 and
 //     geometry.py:150-156; 3D: face normal, |n|, flat-segment test
@@ -35,23 +38,37 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
   constexpr int K = DIM;
   DevState* st = ws.st;
   __shared__ BookShared sb;
-  const BookParams bp = st->bp;
+  __shared__ RoundParams s_rp;
+  __shared__ uint32_t s_seq;
+  if (threadIdx.x == 0) {
+    s_rp = st->rp;
+    s_seq = st->seq;
+    __threadfence();
+    atomicAdd(&st->arrive_book, 1u);  // the finaliser waits for every block's read
+  }
+  __syncthreads();
+  const RoundParams bp = s_rp;
   if (!bp.active) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nsp = bp.nseg_parent;
+  const uint32_t nsp = bp.nseg;
   const uint32_t E = K * nsp;
   const uint32_t num_tiles = (E + TILE3 - 1) / TILE3;
-  const uint32_t tag = bp.tag;
+  const uint32_t tag = s_seq + 1;
   const uint32_t tag16 = (tag % 65535u) + 1u;
   const double eps = st->eps;
   const uint32_t segcap = st->segcap;
   const int64_t stride = st->stride;
+  const uint64_t rcap = ws.rcap;
   const uint32_t in_b = bp.cur, out_b = bp.cur ^ 1u;
   const Seg2* par2 = reinterpret_cast<const Seg2*>(ws.seg[in_b]);
   const Seg3* par3 = reinterpret_cast<const Seg3*>(ws.seg[in_b]);
+  const uint32_t* par_start = ws.segstart[in_b];
+  const uint32_t* cur_in = ws.cursor[in_b];
   Seg2* ch2 = reinterpret_cast<Seg2*>(ws.seg[out_b]);
   Seg3* ch3 = reinterpret_cast<Seg3*>(ws.seg[out_b]);
   uint32_t* segstart = ws.segstart[out_b];
+  uint64_t* seg_phys = ws.seg_phys[out_b];
+  uint32_t* cur_out = ws.cursor[out_b];
   uint32_t* tile_seg = ws.tile_seg[out_b];
 
   while (true) {
@@ -73,7 +90,8 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       v[j].idx = 0;
       v[j].cnt = 0;
       if (e < E) {
-        v[j].cnt = __ldcg(&ws.slot_cnt[e]);
+        const uint32_t p = e / K;
+        v[j].cnt = __ldcg(&cur_in[e]) - __ldg(&par_start[p]);
         if (v[j].cnt) {
           Key128 k = ld_cg(&ws.slot_key[e]);
           v[j].hi = k.hi;
@@ -82,13 +100,12 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
           z.hi = 0;
           z.lo = 0;
           st_cg(&ws.slot_key[e], z);  // slots are all-zero between uses
-          __stcg(&ws.slot_cnt[e], 0u);
         }
       }
       bool occ = v[j].cnt > 0;
       bool emit = occ;
       if (DIM == 3 && occ) {
-        uint32_t s = e / nsp, p = e - s * nsp;
+        uint32_t p = e / K, s = e - p * K;
         const double *A, *B, *C;
         if (bp.root) {  // quickhull.py:359-364
           A = st->pa;
@@ -165,7 +182,7 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
     for (int j = 0; j < ITEMS3; j++) {
       if (!cval[j][0]) continue;
       uint32_t e = base + j * BLOCK + tid;
-      uint32_t s = e / nsp, p = e - s * nsp;
+      uint32_t p = e / K, s = e - p * K;
       const uint32_t* wo = &sb.wsum[(j * WARPS + warp) * 3];
       uint32_t c = sb.prefix.v[0] + wo[0] + ex[j][0];
       uint32_t start = sb.prefix.v[1] + wo[1] + ex[j][1];
@@ -174,8 +191,11 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       if (cval[j][2]) ws.vout[bp.h + vpos] = far;
       if (c >= segcap) continue;  // overflow: reported by the finalising tile
       segstart[c] = start;
+      seg_phys[c] = (uint64_t)s * rcap + __ldg(&par_start[p]);  // where K2 wrote child (p, s)
+#pragma unroll
+      for (int q = 0; q < K; q++) cur_out[(size_t)c * K + q] = start;
       {  // first segment of every next-round tile that starts inside [start, start+cnt)
-        uint32_t t0 = (start + TILE - 1) / TILE, t1 = (start + v[j].cnt - 1) / TILE;
+        uint32_t t0 = (start + RTILE - 1) / RTILE, t1 = (start + v[j].cnt - 1) / RTILE;
         for (uint32_t t = t0; t <= t1; t++) tile_seg[t] = c;
       }
       double F[3];
@@ -237,6 +257,9 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       uint32_t nseg_next = T.v[0], n_next = T.v[1], emitted = T.v[2];
       uint32_t status = st->status;
       uint32_t round_next = bp.round + 1;  // the round the children belong to
+      // every block has read this round's parameters before they change
+      while (*(volatile uint32_t*)&st->arrive_book < gridDim.x) {
+      }
       if (bp.root && DIM == 3) {
         // quickhull.py:349-351 -- every point within eps of the first plane
         double dmax = __longlong_as_double((long long)st->dmax_bits);
@@ -250,6 +273,11 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
         segstart[nseg_next] = n_next;
       }
       if (DIM == 3 && round_next - 1 < MAX_TRACE) st->tr_flat[round_next - 1] = nseg_next - emitted;
+      if (!bp.root && bp.round - 1 < MAX_TRACE) {  // loop round bp.round: (live, kept, segments)
+        st->tr_live[bp.round - 1] = bp.n_live;
+        st->tr_kept[bp.round - 1] = n_next;
+        st->tr_nseg[bp.round - 1] = bp.nseg;
+      }
       uint32_t h_next = bp.h + emitted;
       bool cont = (n_next > 0) && status == ST_OK;
       if (cont && (uint64_t)round_next > (uint64_t)st->n + 1) {  // quickhull.py:227-228
@@ -258,20 +286,19 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       }
       RoundParams rp;
       rp.active = cont ? 1u : 0u;
+      rp.root = 0;
       rp.n_live = n_next;
       rp.nseg = nseg_next;
-      for (int s = 0; s < 4; s++) rp.cnt_in[s] = bp.cnt_out[s];
       rp.cur = out_b;
       rp.h = h_next;
-      rp.round = bp.round;
-      rp.tag = tag + 1;
+      rp.round = round_next;
+      rp.pad = 0;
       st->rp = rp;
       st->status = status;
       st->h_final = h_next;
       st->rounds_final = bp.round;
-      st->seq = tag + 1;
-      st->ctr_round = 0;
-      st->bp.active = 0;
+      st->seq = tag;
+      st->arrive_book = 0;
       if (ws.use_cond) cudaGraphSetConditional(ws.cond, cont ? 1u : 0u);
     }
     __syncthreads();

@@ -2,17 +2,25 @@
 //
 // Data layout in HBM:
 //   * live points of a round are structure-of-arrays records
-//     (x, y[, z] fp64 + uint32 original index) split into K = dim "streams";
-//     stream s holds the survivors whose child state is s, in input order,
-//     so every child segment (s, parent) is one contiguous run.  The next
-//     round reads the K streams back to back ("logical" positions).
+//     (x, y[, z] fp64 + uint32 original index).  Each ping-pong buffer has
+//     K = dim "streams" of capacity rcap; child (p, s) -- the survivors of
+//     segment p with child state s -- is written to stream s at
+//     [segstart[p], segstart[p] + count): disjoint per parent, contiguous per
+//     child, gaps between children.  The next round addresses its segments
+//     through seg_phys (physical element offset of the segment's first
+//     record) and a dense logical numbering (segstart), so it never reads a
+//     gap.  Within a child the order is free (original indices are carried).
+//   * segments are numbered parent-major (child id e = p*K + s), which is the
+//     reference's flat-array segment order (flag_permute's stable (parent,
+//     state) grouping, primitives.py:105-116), so vertices come out in the
+//     reference's discovery order.
 //   * per-segment tables (Seg2 / Seg3) hold everything a point needs to be
 //     classified against its segment's simplex, built once per segment by
 //     the bookkeeping kernel (K3), never per element (the reference gathers
 //     the per-segment edge/face data to every element, quickhull.py:231-233,
 //     :373-375).
-//   * child results (farthest point key + count) are written once per child
-//     into `slots` indexed by the child's stream-order id e = s*nseg + parent.
+//   * per child: a write cursor (survivor count = cursor - parent start) and
+//     the farthest-point key, both merged with atomics.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,6 +37,10 @@ constexpr int TILE = BLOCK * ITEMS;  // 2048 points per tile
 constexpr int ITEMS3 = 4;            // children per thread per tile (bookkeeping kernel)
 constexpr int TILE3 = BLOCK * ITEMS3;
 constexpr int MAX_TRACE = 4096;      // per-round counters kept on device
+constexpr int RB = 128;              // threads per round-kernel block
+constexpr int RITEMS = 8;            // points per thread per round tile
+constexpr int RTILE = RB * RITEMS;   // 1024 points per round tile
+constexpr int WMAX = 256;            // tile-window segments kept in shared memory
 
 // status codes (C ABI, include/seghull_b200.h)
 constexpr uint32_t ST_OK = 0;
@@ -62,37 +74,6 @@ SH_HD RunVal rv_merge(RunVal a, RunVal b) {
   r.hi = take_b ? b.hi : a.hi;
   r.idx = take_b ? b.idx : a.idx;
   r.cnt = a.cnt + b.cnt;
-  return r;
-}
-
-// Look-back payload of one stream over a range of tiles: a reduce-by-key
-// state (segmented reduction over the sorted child keys of that stream).
-struct __align__(16) StreamAgg {
-  uint32_t n;       // elements
-  uint32_t fkey;    // key of the first element
-  uint32_t lkey;    // key of the last element
-  uint32_t single;  // 1 if every element has the same key
-  RunVal lval;      // aggregate of the last run restricted to the range
-};
-
-SH_HD StreamAgg sa_identity() {
-  StreamAgg a;
-  a.n = 0; a.fkey = 0; a.lkey = 0; a.single = 1;
-  a.lval.hi = 0; a.lval.idx = 0xFFFFFFFFu; a.lval.cnt = 0;
-  return a;
-}
-
-// a covers older tiles, b newer ones.
-SH_HD StreamAgg sa_combine(StreamAgg a, StreamAgg b) {
-  if (b.n == 0) return a;
-  if (a.n == 0) return b;
-  StreamAgg r;
-  bool cont = a.lkey == b.fkey;
-  r.n = a.n + b.n;
-  r.fkey = a.fkey;
-  r.lkey = b.lkey;
-  r.single = (a.single && b.single && cont) ? 1u : 0u;
-  r.lval = (b.single && cont) ? rv_merge(a.lval, b.lval) : b.lval;
   return r;
 }
 
@@ -130,30 +111,19 @@ struct __align__(16) Seg3 {
   uint32_t fidx, flat;
 };
 
-// Per-launch parameter blocks.  Each kernel reads only its own block and
-// writes the block of the kernel that follows it, so a finalising tile
-// never changes a value that another tile of the same launch still reads.
-struct RoundParams {      // read by the round kernel (K2)
+// Parameters of one round, read by the round kernel (K2) and the
+// bookkeeping kernel (K3) that follows it.  Only K3's finalising tile
+// writes the next round's parameters, after every K3 block has read them
+// (arrival counter), so no block ever sees a half-updated set.
+struct RoundParams {
   uint32_t active;
+  uint32_t root;          // 1: the first split (K1)
   uint32_t n_live;        // points entering the round (logical positions)
-  uint32_t nseg;          // segments of the round
-  uint32_t cnt_in[4];     // per-stream sizes of the live array
-  uint32_t cur;           // ping-pong index of live records / tables
-  uint32_t h;             // vertices emitted so far
-  uint32_t round;         // rounds completed before this one
-  uint32_t tag;           // look-back tag of this launch
-};
-
-struct BookParams {       // read by the bookkeeping kernel (K3)
-  uint32_t active;
-  uint32_t root;          // 1: children of the first split
-  uint32_t nseg_parent;
-  uint32_t cnt_out[4];    // per-stream survivor counts written by K2
-  uint32_t n_out;
-  uint32_t cur;
-  uint32_t h;
-  uint32_t round;         // rounds completed (children belong to round+1)
-  uint32_t tag;
+  uint32_t nseg;          // segments of the round (parents of its children)
+  uint32_t cur;           // ping-pong index of the buffers the round reads
+  uint32_t h;             // vertices emitted before this round's children
+  uint32_t round;         // 0: first split, r: loop round r
+  uint32_t pad;
 };
 
 struct DevState {
@@ -180,15 +150,14 @@ struct DevState {
   uint64_t dmax_bits;     // 3D coplanarity check: max |d| over the first split
   // ---- loop ----
   RoundParams rp;
-  BookParams bp;
   uint32_t status;
   uint32_t flags;
   uint32_t h_final;
   uint32_t rounds_final;
   uint32_t seg_needed;    // largest segment count requested (overflow retry)
-  uint32_t seq;           // look-back tag, bumped by every finalising tile
-  uint32_t ctr_round;     // dynamic tile counters
-  uint32_t ctr_book;
+  uint32_t seq;           // look-back tag of the bookkeeping kernel
+  uint32_t ctr_book;      // dynamic tile counter of K3 (reset by K2)
+  uint32_t arrive_book;   // K3 blocks that have read rp (reset by K3's finalizer)
   uint32_t ctr_red;       // last-block counter for reductions
   uint32_t pad0;
   // ---- traces (per round r, index r-1) ----
@@ -201,23 +170,22 @@ struct DevState {
 // Device buffers of one context (all allocated once, sized for n / segcap).
 struct Workspace {
   DevState* st;
-  // live records, ping-pong, K regions of capacity rcap each
+  // live records, ping-pong, K streams of capacity rcap each
   double* rx[2];
   double* ry[2];
   double* rz[2];
   uint32_t* ri[2];
   uint64_t rcap;
-  // segment tables (ping-pong)
+  // segment tables (ping-pong, dense segment ids)
   void* seg[2];
-  uint32_t* segstart[2];
-  uint32_t* tile_seg[2];
-  // child results, stream-order ids, zero between uses
-  Key128* slot_key;
-  uint32_t* slot_cnt;
-  // decoupled look-back status words, [tiles][4]
-  uint64_t* lb_round;
+  uint32_t* segstart[2];   // dense logical start (+ sentinel = n_live)
+  uint64_t* seg_phys[2];   // physical element offset of the first record
+  uint32_t* tile_seg[2];   // first segment of every round tile
+  // per child (e = parent*K + state) of the round reading buffer b:
+  uint32_t* cursor[2];     // write cursor, initialised to the parent's start
+  Key128* slot_key;        // farthest key, zero between uses
+  // decoupled look-back status words of K3, [tiles][4]
   uint64_t* lb_book;
-  uint64_t lb_round_words;
   uint64_t lb_book_words;
   // vertex output (uint32 original indices)
   uint32_t* vout;
@@ -226,7 +194,7 @@ struct Workspace {
   uint32_t red_blocks;
   uint32_t round_grid;
   uint32_t book_grid;
-  uint32_t max_tiles;
+  uint32_t max_tiles;     // round tiles at capacity
   cudaGraphConditionalHandle cond;
   uint32_t use_cond;
 };
@@ -300,32 +268,6 @@ __device__ __forceinline__ T shfl_down_t(T v, int off) {
 #pragma unroll
   for (int i = 0; i < (int)(sizeof(T) / 4); i++) d[i] = __shfl_down_sync(0xFFFFFFFFu, s[i], off);
   return r;
-}
-
-// Decoupled look-back (single pass chained scan) over tiles with an
-// NP-wide payload per tile.  Status word: (tag << 2) | flag, flag 1 =
-// aggregate published, 2 = inclusive prefix published.  Payloads are
-// written before the status word (fence in between) and read with .cg
-// loads after it.  Executed by one full warp; returns the exclusive prefix
-// (per payload) in lane 0's `prefix`.
-template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
-__device__ void lookback_publish_agg(uint64_t* flags, P* agg, uint32_t tile, uint32_t tag,
-                                     const P* mine) {
-  int lane = threadIdx.x & 31;
-  if (lane < NP) st_cg(&agg[(size_t)tile * NP + lane], mine[lane]);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_volatile_u64(&flags[tile], ((uint64_t)tag << 2) | 1ull);
-}
-
-template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
-__device__ void lookback_publish_incl(uint64_t* flags, P* incl, uint32_t tile, uint32_t tag,
-                                      const P* mine) {
-  int lane = threadIdx.x & 31;
-  if (lane < NP) st_cg(&incl[(size_t)tile * NP + lane], mine[lane]);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_volatile_u64(&flags[tile], ((uint64_t)tag << 2) | 2ull);
 }
 
 // ------------------------------------------------------------------------
@@ -426,135 +368,6 @@ __device__ __forceinline__ void atomic_max_key(Key128* p, uint64_t hi, uint32_t 
     if (!(hi > old.hi || (hi == old.hi && (unsigned long long)idx < old.lo))) return;
     cmp = old;
   }
-}
-
-// Whole-block look-back: every warp inspects 32 predecessors, so one step
-// covers 32*WARPS tiles in about one L2 round trip.  (A single-warp window
-// caps the tile rate at 32 tiles per round trip, below what HBM needs at
-// 2048-point tiles.)  The window is reduced in parallel: a shuffle tree per
-// warp (older tiles on the left of COMBINE) and a short serial pass over
-// the warp results.  Must be called by all threads of the block; on return
-// s_prefix[0..NP) holds the exclusive prefix of `tile`.
-template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
-__device__ void lookback_block(const uint64_t* flags, const P* agg, const P* incl, uint32_t tile,
-                               uint32_t tag, P* s_warp /*[WARPS*NP]*/, P* s_prefix /*[NP]*/,
-                               int* s_ctl /*[2]*/) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int i = 0; i < NP; i++) s_prefix[i] = IDENT();
-  }
-  int64_t pos = (int64_t)tile - 1;
-  while (pos >= 0) {
-    const int g = warp * 32 + lane;
-    const int64_t t = pos - g;
-    const bool valid = t >= 0;
-    uint32_t fl = 0;
-    if (valid) {
-      uint64_t w;
-      do {
-        w = ld_volatile_u64(&flags[t]);
-      } while ((w >> 2) != (uint64_t)tag || (w & 3ull) == 0);
-      fl = (uint32_t)(w & 3ull);
-    }
-    // nearest inclusive predecessor in the whole window
-    if (threadIdx.x == 0) s_ctl[0] = 1 << 30;
-    __syncthreads();
-    uint32_t im = __ballot_sync(0xFFFFFFFFu, valid && fl == 2);
-    if (lane == 0 && im) atomicMin(&s_ctl[0], warp * 32 + (__ffs(im) - 1));
-    __syncthreads();
-    const int gstop = s_ctl[0];
-    __threadfence();
-    P v[NP];
-    const bool use = valid && g <= gstop;
-#pragma unroll
-    for (int i = 0; i < NP; i++) {
-      v[i] = IDENT();
-      if (use) v[i] = ld_cg(&((fl == 2) ? incl : agg)[(size_t)t * NP + i]);
-    }
-    // shuffle tree: lane l ends with v[l] (+) ... combined over older lanes
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-      for (int i = 0; i < NP; i++) {
-        P o = shfl_down_t(v[i], off);
-        if (lane + off < 32) v[i] = COMBINE(o, v[i]);
-      }
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int i = 0; i < NP; i++) s_warp[warp * NP + i] = v[i];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int i = 0; i < NP; i++) {
-        P w = IDENT();
-        for (int ww = WARPS - 1; ww >= 0; ww--) w = COMBINE(w, s_warp[ww * NP + i]);
-        s_prefix[i] = COMBINE(w, s_prefix[i]);
-      }
-    }
-    __syncthreads();
-    if (gstop < (1 << 30)) break;
-    pos -= 32 * WARPS;
-  }
-}
-
-// window: shared scratch of 32*NP payloads.  On return prefix[0..NP) (all
-// lanes) holds the exclusive prefix of `tile`.
-template <class P, int NP, P (*IDENT)(), P (*COMBINE)(P, P)>
-__device__ void lookback_wait(const uint64_t* flags, const P* agg, const P* incl, uint32_t tile,
-                              uint32_t tag, P* window, P* prefix) {
-  int lane = threadIdx.x & 31;
-  P acc[NP];
-#pragma unroll
-  for (int i = 0; i < NP; i++) acc[i] = IDENT();
-  int64_t pos = (int64_t)tile - 1;
-  while (pos >= 0) {
-    int64_t t = pos - lane;
-    bool valid = t >= 0;
-    uint32_t fl = 0;
-    if (valid) {
-      uint64_t w;
-      do {
-        w = ld_volatile_u64(&flags[t]);
-      } while ((w >> 2) != (uint64_t)tag || (w & 3ull) == 0);
-      fl = (uint32_t)(w & 3ull);
-    }
-    __syncwarp();
-    uint32_t incl_mask = __ballot_sync(0xFFFFFFFFu, valid && fl == 2);
-    uint32_t valid_mask = __ballot_sync(0xFFFFFFFFu, valid);
-    int stop = incl_mask ? (__ffs(incl_mask) - 1) : (31 - __clz(valid_mask));
-    __threadfence();
-    if (lane <= stop) {
-      const P* src = (fl == 2) ? incl : agg;
-#pragma unroll
-      for (int i = 0; i < NP; i++) window[lane * NP + i] = ld_cg(&src[(size_t)t * NP + i]);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      P w[NP];
-#pragma unroll
-      for (int i = 0; i < NP; i++) w[i] = IDENT();
-      for (int l = stop; l >= 0; l--) {
-#pragma unroll
-        for (int i = 0; i < NP; i++) w[i] = COMBINE(w[i], window[l * NP + i]);
-      }
-#pragma unroll
-      for (int i = 0; i < NP; i++) acc[i] = COMBINE(w[i], acc[i]);
-    }
-    __syncwarp();
-    if (incl_mask) break;
-    pos -= 32;
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < NP; i++) window[i] = acc[i];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < NP; i++) prefix[i] = window[i];
-  __syncwarp();
 }
 
 }  // namespace sh

@@ -51,7 +51,7 @@ struct sh_ctx {
   size_t red_bytes = 0;
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[4];
-  int round_occ = 0, book_occ = 0;
+  int round_occ2 = 0, round_occ3 = 0, book_occ = 0;
   uint32_t last_n = 0;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
   // per-launch CUDA events (launch_mode 2): ev[0] before the first launch,
@@ -103,11 +103,11 @@ static void free_ws(sh_ctx* c) {
     cudaFree(w.ri[b]);
     cudaFree(w.seg[b]);
     cudaFree(w.segstart[b]);
+    cudaFree(w.seg_phys[b]);
+    cudaFree(w.cursor[b]);
     cudaFree(w.tile_seg[b]);
   }
   cudaFree(w.slot_key);
-  cudaFree(w.slot_cnt);
-  cudaFree(w.lb_round);
   cudaFree(w.lb_book);
   cudaFree(w.vout);
   cudaFree(w.red);
@@ -133,7 +133,7 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
   const int K = dim;
   uint64_t rcap = n + 16;
   w.rcap = rcap;
-  uint64_t max_tiles = (n + TILE - 1) / TILE + 4;
+  uint64_t max_tiles = (n + RTILE - 1) / RTILE + 4;
   uint64_t book_tiles = ((uint64_t)K * segcap + TILE3 - 1) / TILE3 + 4;
   size_t seg_bytes = (dim == 2) ? sizeof(Seg2) : sizeof(Seg3);
   bool ok = true;
@@ -144,13 +144,12 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
     ok &= dalloc(&w.ri[b], K * rcap) == cudaSuccess;
     ok &= cudaMalloc(&w.seg[b], (size_t)segcap * seg_bytes + 256) == cudaSuccess;
     ok &= dalloc(&w.segstart[b], (size_t)segcap + 4) == cudaSuccess;
+    ok &= dalloc(&w.seg_phys[b], (size_t)segcap + 4) == cudaSuccess;
+    ok &= dalloc(&w.cursor[b], (size_t)K * segcap + 4) == cudaSuccess;
     ok &= dalloc(&w.tile_seg[b], max_tiles + 4) == cudaSuccess;
   }
   ok &= dalloc(&w.slot_key, (size_t)K * segcap + 4) == cudaSuccess;
-  ok &= dalloc(&w.slot_cnt, (size_t)K * segcap + 4) == cudaSuccess;
-  ok &= dalloc(&w.lb_round, max_tiles * 4) == cudaSuccess;
   ok &= dalloc(&w.lb_book, book_tiles * 4) == cudaSuccess;
-  w.lb_round_words = max_tiles * 4;
   w.lb_book_words = book_tiles * 4;
   ok &= dalloc(&w.vout, n + 8) == cudaSuccess;
   w.red_blocks = (uint32_t)c->nsm * 8;
@@ -163,12 +162,10 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
     return set_err(SH_NOMEM, "device allocation failed for the hull workspace");
   }
   CK(cudaMemset(w.slot_key, 0, ((size_t)K * segcap + 4) * sizeof(Key128)));
-  CK(cudaMemset(w.slot_cnt, 0, ((size_t)K * segcap + 4) * sizeof(uint32_t)));
-  CK(cudaMemset(w.lb_round, 0, max_tiles * 4 * sizeof(uint64_t)));
   CK(cudaMemset(w.lb_book, 0, book_tiles * 4 * sizeof(uint64_t)));
   CK(cudaMemset(w.st, 0, sizeof(DevState)));
   w.max_tiles = (uint32_t)max_tiles;
-  w.round_grid = (uint32_t)(c->nsm * c->round_occ);
+  w.round_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round_occ2 : c->round_occ3));
   w.book_grid = (uint32_t)(c->nsm * c->book_occ);
   c->dim = dim;
   c->cap_n = n;
@@ -202,7 +199,7 @@ static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min, uint32
 template <int DIM>
 static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
-  k_round<DIM, false><<<ws.round_grid, BLOCK, dsm, s>>>(ws);
+  k_round<DIM, false><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
@@ -225,7 +222,7 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
     CK(cudaGetLastError());
     prof_mark(c, s, KID_LINE_FAR);
   }
-  k_round<DIM, true><<<ws.round_grid, BLOCK, dsm, s>>>(ws);
+  k_round<DIM, true><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND_FIRST);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
@@ -429,11 +426,11 @@ int sh_create(int device, sh_ctx** out) {
   cudaFuncSetAttribute(k_round<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<3>::bytes());
   int o2 = 0, o3 = 0, ob = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_round<2, false>, BLOCK, RoundSmem<2>::bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_round<3, false>, BLOCK, RoundSmem<3>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_round<2, false>, RB, RoundSmem<2>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_round<3, false>, RB, RoundSmem<3>::bytes());
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
-  // one occupancy for both dims keeps the grids persistent for either
-  c->round_occ = std::max(1, std::min(o2, o3));
+  c->round_occ2 = std::max(1, o2);
+  c->round_occ3 = std::max(1, o3);
   c->book_occ = std::max(1, std::min(ob, 4));
   e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -75,36 +75,47 @@ __device__ __forceinline__ T shfl_xor_t(T v, int m) {
   return r;
 }
 
+// parameters of the first split (K1 + the root bookkeeping)
+__device__ __forceinline__ void start_first_split(DevState* st) {
+  RoundParams rp;
+  rp.active = 1;
+  rp.root = 1;
+  rp.n_live = st->n;
+  rp.nseg = 1;
+  rp.cur = 0;
+  rp.h = st->h_final;
+  rp.round = 0;
+  rp.pad = 0;
+  st->rp = rp;
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
   DevState* st = ws.st;
   // Look-back status words carry a 16-bit launch tag; long before the tag
   // space wraps, zero the status arrays and restart the tags.
   if (st->seq % 65535u >= 32768u) {
-    for (uint64_t i = threadIdx.x; i < ws.lb_round_words; i += blockDim.x) ws.lb_round[i] = 0;
     for (uint64_t i = threadIdx.x; i < ws.lb_book_words; i += blockDim.x) ws.lb_book[i] = 0;
     __syncthreads();
     if (threadIdx.x == 0) st->seq = 0;
     __threadfence();
     __syncthreads();
   }
+  if (threadIdx.x < 4) ws.cursor[0][threadIdx.x] = 0;  // root children start at 0
   if (threadIdx.x == 0) {
-    uint32_t tag = st->seq + 1;
     st->status = ST_OK;
     st->flags = 0;
     st->h_final = 0;
     st->rounds_final = 0;
     st->seg_needed = 0;
     st->first_active = 0;
-    st->ctr_round = 0;
     st->ctr_book = 0;
+    st->arrive_book = 0;
     st->ctr_red = 0;
     st->dmax_bits = 0;
     st->rp.active = 0;
-    st->bp.active = 0;
-    st->bp.tag = tag;   // unused until K1 finalises
-    st->rp.tag = tag;   // tag of K1 (first k_round launch)
-    st->seq = tag;
+    ws.segstart[0][0] = 0;  // the root "parent" of the first split
+    ws.segstart[0][1] = st->n;
   }
 }
 
@@ -228,6 +239,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     // off_line threshold eps * edge_length(pmin, pmax), quickhull.py:203
     st->thr_line = mul(eps, edge_length(t.mn.c[0], t.mn.c[1], t.mx.c[0], t.mx.c[1]));
     st->first_active = 1;
+    start_first_split(st);
   } else {
     st->first_active = (n > 2) ? 2u : 0u;  // 2: K0b runs next
   }
@@ -362,6 +374,7 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
   st->nlen = nlen;
   st->thr_line = mul(-eps, nlen);  // states = d < -eps * nlen (:353)
   st->first_active = 1;
+  start_first_split(st);
 }
 
 }  // namespace sh

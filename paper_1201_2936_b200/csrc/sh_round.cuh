@@ -1,112 +1,75 @@
 // K1/K2: the fused Quickhull round kernel.
 //
-// One persistent launch processes one round over all segments at once.
-// Per 2048-point tile (dynamic tile ids, so look-back never waits on an
-// unscheduled block):
-//   1. coalesced loads of the live records (SoA, K input streams);
-//   2. segment lookup (K3 leaves the first segment of every tile in
-//      tile_seg; the tile's segment starts are staged in shared memory);
-//   3. classification against the segment's simplex -- discard test and
-//      child state in the reference's exact fp64 operation order -- and the
-//      child's next-round distance (the next round's farthest-point key);
-//   4. stable K-way split: warp ballots + a block scan give each survivor
-//      its rank inside its stream; survivors are staged in shared memory in
-//      output order (stream-major, so every child is one contiguous run);
-//   5. reduce-by-key over the staged child keys (warp segmented scans):
-//      farthest point (max distance, lowest original index) and count per
-//      child run.  Runs that start and end inside the tile are final and
-//      written straight to `slots`; the tile's first/last run per stream go
-//      into the look-back payload;
-//   6. decoupled look-back: stream offsets + the open run carried across
-//      tiles (sa_combine), so a child split across tiles is closed by the
-//      first tile that sees its end -- no global atomics at all;
-//   7. coalesced copy-out of the staged records to the output streams.
+// One launch processes one whole round over all segments at once, reading
+// every live record once and writing every survivor once
+// (quickhull.py:229-266 / :372-437; the first split :200-222 / :346-364 is
+// the FIRST instantiation).
+//
+// Work split: persistent blocks, each owning a static contiguous range of
+// 1024-point tiles.  Tiles are independent -- there is no tile-to-tile
+// prefix chain: every child (parent segment p, state s) owns a disjoint
+// region of output stream s starting at p's start, and survivors claim
+// positions in it with one shared-memory atomic per warp and one global
+// atomicAdd per (tile, child).  Order inside a child is free because
+// records carry their original index.
+//
+// Per tile:
+//   * the records were prefetched into shared memory with cp.async while the
+//     previous tile was processed (double buffering); the tile's segment
+//     window (start, physical offset of every segment overlapping the tile)
+//     is staged in shared memory;
+//   * classification against the segment's simplex in the reference's fp64
+//     operation order: discard test, child state, and the child's distance
+//     for the next round (the next round's farthest-point key);
+//   * per-child counts and farthest keys: warp ballots + REDUX reductions
+//     when a 32-point slot lies in one segment (the common case), shared
+//     atomics otherwise; then one global cursor claim per child;
+//   * survivors are written straight from the staged records;
+//   * a child's farthest key is stored directly when the child lies inside
+//     one tile, carried to the block's next tile when its segment continues,
+//     and merged with a 128-bit atomicCAS when several blocks share it.
+// Windows wider than WMAX segments (late rounds of tiny segments) take a
+// slow path with per-point global atomics.
 #pragma once
 
 #include "sh_common.cuh"
 
 namespace sh {
 
-struct Frag {
-  uint32_t has, single, fkey, lkey;
-  RunVal fval, lval;
-};
+constexpr uint32_t NOKEY = 0xFFFFFFFFu;
 
 template <int DIM>
 struct RoundSmem {
-  // dynamic part: staging (union with the segment-start window)
-  static constexpr size_t bytes() {
-    return (size_t)TILE * (8 * DIM + 8 + 4 + 4) + 64;
-  }
+  // one stage: DIM coordinate arrays, original index, window index
+  static constexpr size_t stage_bytes() { return (size_t)RTILE * (8 * DIM + 4 + 2); }
+  static constexpr size_t bytes() { return 2 * stage_bytes(); }
 };
 
+template <int DIM>
 struct RoundShared {
-  uint32_t tile;
-  uint32_t nwin;
-  uint32_t seg_lo;
-  uint32_t last;
-  uint32_t off[5];
-  uint32_t wcnt[ITEMS * WARPS * 3];
-  uint32_t fkey[3], lkey[3];
-  RunVal first[3], last_run[3];
-  uint32_t cnt[4], prefix[4], incl[4];
-  int stop[4];
-  // per-block pending run per stream, carried across the block's tiles
-  uint32_t pend_key[3];
-  uint32_t pend_valid[3];
-  RunVal pend[3];
-  Frag frag[WARPS];
+  uint32_t wstart[2][WMAX + 2];      // window: dense start of every segment (+ next)
+  unsigned long long wphys[2][WMAX + 1];  // window: physical offset of every segment
+  uint32_t wlo[2], wn[2], wslow[2];
+  uint32_t kcnt[WMAX * DIM];         // per (window segment, state) of the current tile
+  uint32_t kbase[WMAX * DIM];
+  unsigned long long khi[WMAX * DIM];
+  uint32_t kidx[WMAX * DIM];
+  uint32_t pend_seg[2];              // segment carried into the next tile (by tile parity)
+  uint32_t pend_complete[2];         // its aggregate covers it from its first point
+  unsigned long long pend_hi[2][DIM];
+  uint32_t pend_idx[2][DIM];
 };
 
-__device__ __forceinline__ RunVal rv_ident() {
-  RunVal r;
-  r.hi = 0;
-  r.idx = 0xFFFFFFFFu;
-  r.cnt = 0;
-  return r;
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
-
-template <int K>
-__device__ __forceinline__ void flush_run(RoundShared& sh_, const Workspace& ws, uint32_t nseg,
-                                          uint32_t key, RunVal v) {
-  uint32_t s = (K == 1) ? 0 : key / nseg;
-  bool done = false;
-  if (key == sh_.fkey[s]) {
-    sh_.first[s] = v;
-    done = true;
-  }
-  if (key == sh_.lkey[s]) {
-    sh_.last_run[s] = v;
-    done = true;
-  }
-  if (!done) {
-    // a run bounded by other keys inside the tile is the whole child
-    Key128 k;
-    k.hi = v.hi;
-    k.lo = v.idx;
-    st_cg(&ws.slot_key[key], k);
-    ws.slot_cnt[key] = v.cnt;
-  }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
 }
-
-// Boundary runs of a child that spans tiles: merged with atomics.
-__device__ __forceinline__ void flush_atomic(const Workspace& ws, uint32_t key, RunVal v) {
-  atomicAdd(&ws.slot_cnt[key], v.cnt);
-  atomic_max_key(&ws.slot_key[key], v.hi, v.idx);
-}
-
-// Thread 0: fold a boundary run into the block's pending run of its stream.
-__device__ __forceinline__ void pend_push(RoundShared& sh_, const Workspace& ws, int s, uint32_t key,
-                                          RunVal v) {
-  if (sh_.pend_valid[s] && sh_.pend_key[s] == key) {
-    sh_.pend[s] = rv_merge(sh_.pend[s], v);
-  } else {
-    if (sh_.pend_valid[s]) flush_atomic(ws, sh_.pend_key[s], sh_.pend[s]);
-    sh_.pend_key[s] = key;
-    sh_.pend[s] = v;
-    sh_.pend_valid[s] = 1;
-  }
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Classification of one point against its segment (2D), quickhull.py:230-266.
 // Returns state in {-1 (discard), 0, 1} and the child's next-round distance.
@@ -150,41 +113,33 @@ __device__ __forceinline__ int classify3(const Seg3& g, double qx, double qy, do
   return state;
 }
 
+// largest w in [0, n) with start[w] <= q
+__device__ __forceinline__ uint32_t win_search(const uint32_t* start, uint32_t n, uint32_t q) {
+  uint32_t lo = 0, hi = n - 1;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= q) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 template <int DIM, bool FIRST>
-__global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
+__global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   constexpr int K = DIM;
   DevState* st = ws.st;
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ RoundShared sh_;
-  double* sx = reinterpret_cast<double*>(dsm);
-  double* sy = sx + TILE;
-  double* sz = sy + TILE;  // DIM == 3 only
-  uint64_t* shi = reinterpret_cast<uint64_t*>(sx + DIM * TILE);
-  uint32_t* sidx = reinterpret_cast<uint32_t*>(shi + TILE);
-  uint32_t* skey = sidx + TILE;
-  uint32_t* swin = reinterpret_cast<uint32_t*>(dsm);  // union with staging
+  __shared__ RoundShared<DIM> S;
+  const int tid = threadIdx.x, lane = tid & 31;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  // ---- launch parameters (own block only, see RoundParams)
-  uint32_t n_live, nseg, cur, tag;
-  uint32_t cum1 = 0, cum2 = 0;
-  if (FIRST) {
-    if (st->first_active != 1) return;
-    n_live = st->n;
-    nseg = 1;
-    cur = 0;
-    tag = st->rp.tag;
-  } else {
-    if (!st->rp.active) return;
-    n_live = st->rp.n_live;
-    nseg = st->rp.nseg;
-    cur = st->rp.cur;
-    tag = st->rp.tag;
-    cum1 = st->rp.cnt_in[0];
-    cum2 = cum1 + st->rp.cnt_in[1];
-  }
-  const uint32_t num_tiles = (n_live + TILE - 1) / TILE;
+  const RoundParams rp = st->rp;
+  if (!rp.active || (rp.root != 0) != FIRST) return;
+  if (blockIdx.x == 0 && tid == 0) st->ctr_book = 0;  // K3's tile counter
+  const uint32_t n_live = rp.n_live, nseg = rp.nseg, cur = rp.cur;
+  const uint32_t num_tiles = (n_live + RTILE - 1) / RTILE;
+  const uint32_t t0 = (uint32_t)(((uint64_t)num_tiles * blockIdx.x) / gridDim.x);
+  const uint32_t t1 = (uint32_t)(((uint64_t)num_tiles * (blockIdx.x + 1)) / gridDim.x);
+  if (t0 >= t1) return;
   const uint64_t rcap = ws.rcap;
   const double* inx = ws.rx[cur];
   const double* iny = ws.ry[cur];
@@ -195,13 +150,21 @@ __global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
   double* outz = ws.rz[cur ^ 1u];
   uint32_t* outi = ws.ri[cur ^ 1u];
   const uint32_t* segstart = ws.segstart[cur];
+  const uint64_t* seg_phys = ws.seg_phys[cur];
   const uint32_t* tile_seg = ws.tile_seg[cur];
   const Seg2* seg2 = reinterpret_cast<const Seg2*>(ws.seg[cur]);
   const Seg3* seg3 = reinterpret_cast<const Seg3*>(ws.seg[cur]);
+  uint32_t* cursor = ws.cursor[cur];
+  const uint32_t block_begin = t0 * RTILE;
+  const uint32_t block_end = min(t1 * RTILE, n_live);
 
   // first-split constants
   double f_pa[3], f_pb[3], f_nrm[3], f_thr = 0;
   uint32_t f_imin = 0, f_imax = 0, f_ifar = 0xFFFFFFFFu;
+  const double* px = st->px;
+  const double* py = st->py;
+  const double* pz = st->pz;
+  const int64_t pstride = st->stride;
   if (FIRST) {
 #pragma unroll
     for (int k = 0; k < 3; k++) {
@@ -215,351 +178,293 @@ __global__ void __launch_bounds__(BLOCK, 2) k_round(Workspace ws) {
     if (DIM == 3) f_ifar = st->ifar;
   }
   double dmax_local = 0.0;
-  const uint32_t tag16 = (tag % 65535u) + 1u;
-  if (tid < 3) sh_.pend_valid[tid] = 0;
 
-  while (true) {
-    if (tid == 0) sh_.tile = atomicAdd(&st->ctr_round, 1u);
-    __syncthreads();
-    const uint32_t tile = sh_.tile;
-    if (tile >= num_tiles) break;
-    const uint32_t base = tile * TILE;
-    const bool last_tile = (tile == num_tiles - 1);
+  auto stage_ptr = [&](uint32_t b) { return dsm + (size_t)b * RoundSmem<DIM>::stage_bytes(); };
 
-    // ---- segment window
-    if (!FIRST) {
-      if (tid == 0) {
-        uint32_t lo = tile_seg[tile];
-        uint32_t hi = (tile + 1 < num_tiles) ? tile_seg[tile + 1] : nseg - 1;
-        sh_.seg_lo = lo;
-        sh_.nwin = hi - lo + 1;
+  // ---- window of tile t into buffer b (warp 0)
+  auto load_window = [&](uint32_t t, uint32_t b) {
+    if (FIRST) {
+      if (lane == 0) {
+        S.wlo[b] = 0;
+        S.wn[b] = 1;
+        S.wslow[b] = 0;
+        S.wstart[b][0] = 0;
+        S.wstart[b][1] = n_live;
+        S.wphys[b][0] = 0;
       }
-      __syncthreads();
-      for (uint32_t i = tid; i < sh_.nwin; i += BLOCK) swin[i] = segstart[sh_.seg_lo + i];
-      __syncthreads();
+      return;
     }
-    const uint32_t seg_lo = FIRST ? 0u : sh_.seg_lo;
-    const uint32_t nwin = FIRST ? 1u : sh_.nwin;
+    const uint32_t lo = tile_seg[t];
+    const uint32_t hi = (t + 1 < num_tiles) ? tile_seg[t + 1] : nseg - 1;
+    const uint32_t nw = hi - lo + 1;
+    const bool slow = nw > (uint32_t)WMAX;
+    if (!slow) {
+      for (uint32_t w = lane; w <= nw; w += 32) S.wstart[b][w] = segstart[lo + w];
+      for (uint32_t w = lane; w < nw; w += 32) S.wphys[b][w] = seg_phys[lo + w];
+    }
+    if (lane == 0) {
+      S.wlo[b] = lo;
+      S.wn[b] = nw;
+      S.wslow[b] = slow ? 1u : 0u;
+    }
+  };
 
-    // ---- load + classify (striped: item j of thread t is base + j*BLOCK + t)
-    double qx[ITEMS], qy[ITEMS], qz[ITEMS];
-    uint32_t qi[ITEMS], qseg[ITEMS];
-    int qs[ITEMS];
-    uint64_t qhi[ITEMS];
+  // ---- cp.async the records of tile t into stage b (all threads; window b ready)
+  auto issue_items = [&](uint32_t t, uint32_t b) {
+    unsigned char* sp = stage_ptr(b);
+    double* sx = reinterpret_cast<double*>(sp);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sx + DIM * RTILE);
+    uint16_t* sw = reinterpret_cast<uint16_t*>(si + RTILE);
+    const uint32_t base = t * RTILE;
+    const uint32_t lo = S.wlo[b], nw = S.wn[b];
+    const bool slow = S.wslow[b] != 0;
 #pragma unroll
-    for (int j = 0; j < ITEMS; j++) {
-      uint32_t p = base + j * BLOCK + tid;
-      qs[j] = -1;
-      qseg[j] = 0;
-      qi[j] = p;
-      qx[j] = qy[j] = qz[j] = 0.0;
-      if (p < n_live) {
-        if (FIRST) {
-          qx[j] = ld_coord(st->px, st->stride, p);
-          qy[j] = ld_coord(st->py, st->stride, p);
-          if (DIM == 3) qz[j] = ld_coord(st->pz, st->stride, p);
+    for (int j = 0; j < RITEMS; j++) {
+      const uint32_t i = j * RB + tid;
+      const uint32_t q = base + i;
+      if (q >= n_live) continue;
+      if (FIRST) {
+        const int64_t o = (int64_t)q * pstride;
+        cp_async8(&sx[i], px + o);
+        cp_async8(&sx[RTILE + i], py + o);
+        if (DIM == 3) cp_async8(&sx[2 * RTILE + i], pz + o);
+        sw[i] = 0;
+      } else {
+        uint32_t w;
+        uint64_t phys;
+        if (!slow) {
+          w = win_search(S.wstart[b], nw, q);
+          phys = S.wphys[b][w] + (q - S.wstart[b][w]);
         } else {
-          uint32_t s = (p >= cum1) + (K == 3 ? (p >= cum2) : 0);
-          uint32_t o = p - (s == 0 ? 0u : (s == 1 ? cum1 : cum2));
-          size_t a = (size_t)s * rcap + o;
-          qx[j] = __ldcs(inx + a);
-          qy[j] = __ldcs(iny + a);
-          if (DIM == 3) qz[j] = __ldcs(inz + a);
-          qi[j] = __ldcs(ini + a);
+          w = win_search(segstart + lo, nw, q);
+          phys = seg_phys[lo + w] + (q - segstart[lo + w]);
         }
+        sw[i] = (uint16_t)w;
+        cp_async8(&sx[i], inx + phys);
+        cp_async8(&sx[RTILE + i], iny + phys);
+        if (DIM == 3) cp_async8(&sx[2 * RTILE + i], inz + phys);
+        cp_async4(&si[i], ini + phys);
       }
     }
+    cp_async_commit();
+  };
+
+  // ---- prologue
+  if (tid < K * WMAX) {
+    for (uint32_t e = tid; e < (uint32_t)(K * WMAX); e += RB) {
+      S.kcnt[e] = 0;
+      S.khi[e] = 0ull;
+      S.kidx[e] = 0xFFFFFFFFu;
+    }
+  }
+  if (tid < 2) {
+    S.pend_seg[tid] = NOKEY;
+    S.pend_complete[tid] = 0;
+  }
+  if (tid < 32) load_window(t0, 0);
+  __syncthreads();
+  issue_items(t0, 0);
+
+  for (uint32_t t = t0; t < t1; t++) {
+    const uint32_t lt = t - t0;
+    const uint32_t b = lt & 1u;
+    const bool has_next = t + 1 < t1;
+    if (has_next && tid < 32) load_window(t + 1, b ^ 1u);
+    cp_async_wait_all();
+    __syncthreads();  // stage b landed, window b^1 staged
+    if (has_next) issue_items(t + 1, b ^ 1u);
+
+    const uint32_t tile_begin = t * RTILE;
+    const uint32_t tile_end = min(tile_begin + RTILE, n_live);
+    const uint32_t lo = S.wlo[b], nw = S.wn[b];
+    const bool slow = S.wslow[b] != 0;
+    unsigned char* sp = stage_ptr(b);
+    const double* sx = reinterpret_cast<const double*>(sp);
+    const uint32_t* si = reinterpret_cast<const uint32_t*>(sx + DIM * RTILE);
+    const uint16_t* sw = reinterpret_cast<const uint16_t*>(si + RTILE);
+    const uint32_t pin = (lt + 1u) & 1u;  // pending written by the previous tile
+    const uint32_t pout = lt & 1u;
+
+    // ---- classify
+    uint32_t key[RITEMS], rank[RITEMS];
+    unsigned long long khi_[RITEMS];
 #pragma unroll
-    for (int j = 0; j < ITEMS; j++) {
-      uint32_t p = base + j * BLOCK + tid;
-      if (p >= n_live) continue;
+    for (int j = 0; j < RITEMS; j++) {
+      const uint32_t i = j * RB + tid;
+      const uint32_t q = tile_begin + i;
+      key[j] = NOKEY;
+      rank[j] = 0;
+      khi_[j] = 0;
+      if (q >= tile_end) continue;
+      const double qx = sx[i], qy = sx[RTILE + i];
+      const double qz = (DIM == 3) ? sx[2 * RTILE + i] : 0.0;
+      const uint32_t w = sw[i];
       double dn = 0.0;
       int s = -1;
       if (FIRST) {
         if (DIM == 2) {
-          if (p != f_imin && p != f_imax) {
+          if (q != f_imin && q != f_imax) {
             // quickhull.py:202-211
-            double d = cross2(f_pa[0], f_pa[1], f_pb[0], f_pb[1], qx[j], qy[j]);
+            double d = cross2(f_pa[0], f_pa[1], f_pb[0], f_pb[1], qx, qy);
             if (fabs(d) > f_thr) {
               s = d < 0 ? 1 : 0;
               dn = s ? -d : d;  // cross2(pmax, pmin, q) == -d exactly
             }
           }
         } else {
-          if (p != f_imin && p != f_imax && p != f_ifar) {
+          if (q != f_imin && q != f_imax && q != f_ifar) {
             // quickhull.py:348-353
-            double d = plane_dist(f_nrm, f_pa, qx[j], qy[j], qz[j]);
+            double d = plane_dist(f_nrm, f_pa, qx, qy, qz);
             dmax_local = fmax(dmax_local, fabs(d));
             s = d < f_thr ? 1 : 0;
             dn = s ? -d : d;  // face (pa, pc, pb) has normal -n exactly
           }
         }
       } else {
-        // segment: largest w with swin[w] <= p
-        uint32_t lo = 0, hi = nwin - 1;
-        while (lo < hi) {
-          uint32_t mid = (lo + hi + 1) >> 1;
-          if (swin[mid] <= p) lo = mid;
-          else hi = mid - 1;
-        }
-        uint32_t sg = seg_lo + lo;
-        qseg[j] = sg;
-        if (DIM == 2) s = classify2(seg2[sg], qx[j], qy[j], qi[j], &dn);
-        else s = classify3(seg3[sg], qx[j], qy[j], qz[j], qi[j], &dn);
+        const uint32_t qi = si[i];
+        if (DIM == 2) s = classify2(seg2[lo + w], qx, qy, qi, &dn);
+        else s = classify3(seg3[lo + w], qx, qy, qz, qi, &dn);
       }
-      qs[j] = s;
-      qhi[j] = ordered_bits(dn);
-    }
-
-    // ---- stable K-way split: ranks inside the tile
-    uint32_t lrank[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; j++) {
-      lrank[j] = 0;
-#pragma unroll
-      for (int s = 0; s < K; s++) {
-        uint32_t m = __ballot_sync(0xFFFFFFFFu, qs[j] == s);
-        if (qs[j] == s) lrank[j] = __popc(m & lanemask_lt());
-        if (lane == 0) sh_.wcnt[(j * WARPS + warp) * 3 + s] = __popc(m);
+      if (s >= 0) {
+        key[j] = w * K + (uint32_t)s;
+        khi_[j] = ordered_bits(dn);
       }
     }
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t tot_prev = 0;
-#pragma unroll
-      for (int s = 0; s < K; s++) {
-        uint32_t a = sh_.wcnt[(2 * lane) * 3 + s];
-        uint32_t b = sh_.wcnt[(2 * lane + 1) * 3 + s];
-        uint32_t v = a + b;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, off);
-          if (lane >= off) v += o;
-        }
-        uint32_t ex = v - a - b;
-        sh_.wcnt[(2 * lane) * 3 + s] = ex;
-        sh_.wcnt[(2 * lane + 1) * 3 + s] = ex + a;
-        uint32_t tot = __shfl_sync(0xFFFFFFFFu, v, 31);
-        if (lane == 0) sh_.off[s] = tot_prev;
-        tot_prev += tot;
-      }
-      if (lane == 0) sh_.off[K] = tot_prev;
-    }
-    __syncthreads();
 
-    // ---- stage survivors in output order (the window is no longer needed)
-    const uint32_t N = sh_.off[K];
+    if (!slow) {
+      // ---- per (segment, state): tile-local ranks, counts, farthest keys
 #pragma unroll
-    for (int j = 0; j < ITEMS; j++) {
-      int s = qs[j];
-      if (s < 0) continue;
-      uint32_t pos = sh_.off[s] + sh_.wcnt[(j * WARPS + warp) * 3 + s] + lrank[j];
-      sx[pos] = qx[j];
-      sy[pos] = qy[j];
-      if (DIM == 3) sz[pos] = qz[j];
-      sidx[pos] = qi[j];
-      shi[pos] = qhi[j];
-      skey[pos] = (uint32_t)s * nseg + qseg[j];
-    }
-    __syncthreads();
-    if (tid < K) {
-      uint32_t a = sh_.off[tid], b = sh_.off[tid + 1];
-      sh_.fkey[tid] = (b > a) ? skey[a] : 0xFFFFFFFFu;
-      sh_.lkey[tid] = (b > a) ? skey[b - 1] : 0xFFFFFFFFu;
-      sh_.first[tid] = rv_ident();
-      sh_.last_run[tid] = rv_ident();
-    }
-    __syncthreads();
-
-    // ---- reduce-by-key over staged child keys (per warp, 32 at a time)
-    {
-      uint32_t chunk = (((N + WARPS - 1) / WARPS) + 31u) & ~31u;
-      uint32_t w0 = min(N, warp * chunk), w1 = min(N, w0 + chunk);
-      Frag fr;
-      fr.has = (w1 > w0);
-      fr.single = 1;
-      fr.fkey = fr.lkey = 0;
-      fr.fval = fr.lval = rv_ident();
-      bool first_open = true, carry_valid = false;
-      uint32_t carry_key = 0;
-      RunVal carry = rv_ident();
-      for (uint32_t cb = w0; cb < w1; cb += 32) {
-        uint32_t e = cb + lane;
-        bool valid = e < w1;
-        uint32_t key = valid ? skey[e] : 0xFFFFFFFFu;
-        RunVal v = rv_ident();
-        if (valid) {
-          v.hi = shi[e];
-          v.idx = sidx[e];
-          v.cnt = 1;
-        }
-        uint32_t prevk = __shfl_up_sync(0xFFFFFFFFu, key, 1);
-        uint32_t nextk = __shfl_down_sync(0xFFFFFFFFu, key, 1);
-        bool head = (lane == 0) || (key != prevk);
-        RunVal val = v;
-        bool f = head;
+      for (int j = 0; j < RITEMS; j++) {
+        const uint32_t i = j * RB + tid;
+        const bool valid = tile_begin + i < tile_end;
+        const uint32_t w = valid ? (uint32_t)sw[i] : 0u;
+        const uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, valid ? w : 0xFFFFu);
+        const uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, valid ? w : 0u);
+        if (wmin == wmax) {
+          // one segment in this 32-point slot: ballots + REDUX per state
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          RunVal ov = shfl_up_t(val, off);
-          bool of = __shfl_up_sync(0xFFFFFFFFu, f, off);
-          if (lane >= off) {
-            if (!f) val = rv_merge(ov, val);
-            f = f || of;
+          for (int s = 0; s < K; s++) {
+            const uint32_t kk = wmin * K + s;
+            const bool mine = key[j] == kk;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+            if (!m) continue;
+            const uint32_t hu = mine ? (uint32_t)(khi_[j] >> 32) : 0u;
+            const uint32_t mu = __reduce_max_sync(0xFFFFFFFFu, hu);
+            const uint32_t hl = (mine && hu == mu) ? (uint32_t)khi_[j] : 0u;
+            const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, hl);
+            const int leader = __ffs(m) - 1;
+            uint32_t off = 0;
+            if (lane == leader) {
+              off = atomicAdd(&S.kcnt[kk], (uint32_t)__popc(m));
+              atomicMax(&S.khi[kk], ((unsigned long long)mu << 32) | ml);
+            }
+            off = __shfl_sync(0xFFFFFFFFu, off, leader);
+            if (mine) rank[j] = off + __popc(m & lanemask_lt());
           }
-        }
-        int lastl = (int)min(31u, w1 - 1 - cb);
-        bool tail = valid && (lane == lastl || nextk != key);
-        uint32_t tail_mask = __ballot_sync(0xFFFFFFFFu, tail);
-        int first_tail = __ffs(tail_mask) - 1;
-        uint32_t k0 = __shfl_sync(0xFFFFFFFFu, key, 0);
-        // the chunk's first run continues the carry?
-        bool cont = carry_valid && carry_key == k0;
-        bool closeA = carry_valid && !cont;
-        if (tail && lane == first_tail && cont) val = rv_merge(carry, val);
-        uint32_t closeB = __ballot_sync(0xFFFFFFFFu, tail && lane != lastl);
-        if (first_open) {
-          if (closeA) {
-            fr.fkey = carry_key;
-            fr.fval = carry;
-            first_open = false;
-          } else if (closeB) {
-            int fl = __ffs(closeB) - 1;
-            fr.fkey = __shfl_sync(0xFFFFFFFFu, key, fl);
-            fr.fval = shfl_t(val, fl);
-            closeB &= closeB - 1;  // that run is recorded, not flushed
-            first_open = false;
-          }
-        } else if (closeA) {
-          if (lane == 0) flush_run<K>(sh_, ws, nseg, carry_key, carry);
-        }
-        if ((closeB >> lane) & 1u) flush_run<K>(sh_, ws, nseg, key, val);
-        carry_key = __shfl_sync(0xFFFFFFFFu, key, lastl);
-        carry = shfl_t(val, lastl);
-        carry_valid = true;
-      }
-      if (fr.has) {
-        fr.lkey = carry_key;
-        fr.lval = carry;
-        if (first_open) {
-          fr.single = 1;
-          fr.fkey = carry_key;
-          fr.fval = carry;
         } else {
-          fr.single = 0;
+          const uint32_t grp = __match_any_sync(0xFFFFFFFFu, key[j]);
+          const int leader = __ffs(grp) - 1;
+          uint32_t off = 0;
+          if (key[j] != NOKEY && lane == leader) off = atomicAdd(&S.kcnt[key[j]], (uint32_t)__popc(grp));
+          off = __shfl_sync(0xFFFFFFFFu, off, leader);
+          if (key[j] != NOKEY) {
+            rank[j] = off + __popc(grp & lanemask_lt());
+            atomicMax(&S.khi[key[j]], khi_[j]);
+          }
         }
       }
-      if (lane == 0) sh_.frag[warp] = fr;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      Frag A = sh_.frag[0];
-      for (int w = 1; w < WARPS; w++) {
-        Frag F = sh_.frag[w];
-        if (!F.has) continue;
-        if (!A.has) {
-          A = F;
-          continue;
+      __syncthreads();
+      // ---- lowest index among the farthest; one global claim per child
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) {
+        if (key[j] != NOKEY && khi_[j] == S.khi[key[j]])
+          atomicMin(&S.kidx[key[j]], FIRST ? tile_begin + j * RB + tid : si[j * RB + tid]);
+      }
+      const uint32_t ne = nw * K;
+      for (uint32_t e = tid; e < ne; e += RB) {
+        const uint32_t c = S.kcnt[e];
+        if (c) S.kbase[e] = atomicAdd(&cursor[(size_t)(lo + e / K) * K + e % K], c);
+      }
+      __syncthreads();
+      // ---- write the survivors
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) {
+        if (key[j] == NOKEY) continue;
+        const uint32_t i = j * RB + tid;
+        const uint32_t s = key[j] % K;
+        const size_t dst = (size_t)s * rcap + S.kbase[key[j]] + rank[j];
+        outx[dst] = sx[i];
+        outy[dst] = sx[RTILE + i];
+        if (DIM == 3) outz[dst] = sx[2 * RTILE + i];
+        outi[dst] = FIRST ? (tile_begin + i) : si[i];
+      }
+      // ---- close, carry or merge every child of the tile
+      for (uint32_t e = tid; e < ne; e += RB) {
+        const uint32_t w = e / K, s = e % K;
+        const uint32_t seg = lo + w;
+        const uint32_t segbeg = S.wstart[b][w], segend = S.wstart[b][w + 1];
+        unsigned long long hi = S.kcnt[e] ? S.khi[e] : 0ull;
+        uint32_t idx = S.kidx[e];
+        bool complete = segbeg >= tile_begin;
+        if (w == 0 && S.pend_seg[pin] == seg) {
+          const unsigned long long ph = S.pend_hi[pin][s];
+          const uint32_t pi = S.pend_idx[pin][s];
+          if (ph > hi || (ph == hi && pi < idx)) {
+            hi = ph;
+            idx = pi;
+          }
+          complete = S.pend_complete[pin] != 0;
         }
-        if (A.lkey == F.fkey) {
-          RunVal m = rv_merge(A.lval, F.fval);
-          if (A.single && F.single) {
-            A.fval = m;
-            A.lval = m;
-          } else if (A.single) {
-            A.fval = m;
-            A.lkey = F.lkey;
-            A.lval = F.lval;
-            A.single = 0;
-          } else if (F.single) {
-            A.lval = m;
+        const bool continues = segend > tile_end;
+        if (continues && has_next && w == nw - 1) {
+          S.pend_hi[pout][s] = hi;
+          S.pend_idx[pout][s] = idx;
+          if (s == 0) {
+            S.pend_seg[pout] = seg;
+            S.pend_complete[pout] = complete ? 1u : 0u;
+          }
+        } else if (hi) {
+          Key128* slot = &ws.slot_key[(size_t)seg * K + s];
+          if (complete && !continues) {
+            Key128 kv;
+            kv.hi = hi;
+            kv.lo = idx;
+            st_cg(slot, kv);
           } else {
-            flush_run<K>(sh_, ws, nseg, A.lkey, m);
-            A.lkey = F.lkey;
-            A.lval = F.lval;
+            atomic_max_key(slot, hi, idx);
           }
-        } else {
-          if (!A.single) flush_run<K>(sh_, ws, nseg, A.lkey, A.lval);
-          if (!F.single) flush_run<K>(sh_, ws, nseg, F.fkey, F.fval);
-          A.lkey = F.lkey;
-          A.lval = F.lval;
-          A.single = 0;
         }
+        S.kcnt[e] = 0;
+        S.khi[e] = 0ull;
+        S.kidx[e] = 0xFFFFFFFFu;
       }
-      if (A.has) {
-        flush_run<K>(sh_, ws, nseg, A.fkey, A.fval);
-        if (!A.single) flush_run<K>(sh_, ws, nseg, A.lkey, A.lval);
+      if (tid == 0 && !(has_next && S.wstart[b][nw] > tile_end)) S.pend_seg[pout] = NOKEY;
+    } else {
+      // ---- slow path: per-point global claims (windows wider than WMAX)
+      if (tid < K && S.pend_seg[pin] != NOKEY) {
+        const unsigned long long ph = S.pend_hi[pin][tid];
+        if (ph) atomic_max_key(&ws.slot_key[(size_t)S.pend_seg[pin] * K + tid], ph, S.pend_idx[pin][tid]);
       }
-    }
-    __syncthreads();
-
-    // ---- stream offsets: count-only decoupled look-back (whole block)
-    if (tid < K) sh_.cnt[tid] = sh_.off[tid + 1] - sh_.off[tid];
-    __syncthreads();
-    if (tile > 0) {
-      if (tid == 0) lb_publish<K>(ws.lb_round, tile, tag16, LB_AGG, sh_.cnt);
-      lb_lookback<K>(ws.lb_round, tile, tag16, sh_.prefix, sh_.stop);
-    } else if (tid < K) {
-      sh_.prefix[tid] = 0;
-    }
-    __syncthreads();
-    if (tid == 0) {
+      if (tid == 0) S.pend_seg[pout] = NOKEY;
 #pragma unroll
-      for (int s = 0; s < K; s++) sh_.incl[s] = sh_.prefix[s] + sh_.cnt[s];
-      lb_publish<K>(ws.lb_round, tile, tag16, LB_INC, sh_.incl);
-      // tile-boundary runs of children that may span tiles: merge into the
-      // block's pending run (children are contiguous, so consecutive tiles
-      // of a long child keep hitting the same pending run)
-#pragma unroll
-      for (int s = 0; s < K; s++) {
-        if (sh_.cnt[s] == 0) continue;
-        pend_push(sh_, ws, s, sh_.fkey[s], sh_.first[s]);
-        if (sh_.lkey[s] != sh_.fkey[s]) pend_push(sh_, ws, s, sh_.lkey[s], sh_.last_run[s]);
-      }
-      // ---- finalise the launch
-      if (last_tile) {
-        uint32_t tot = 0;
-        BookParams bp;
-        bp.active = 1;
-        bp.root = FIRST ? 1u : 0u;
-        bp.nseg_parent = nseg;
-        for (int s = 0; s < 4; s++) bp.cnt_out[s] = (s < K) ? sh_.incl[s] : 0u;
-        for (int s = 0; s < K; s++) tot += sh_.incl[s];
-        bp.n_out = tot;
-        bp.cur = cur;
-        bp.h = FIRST ? st->h_final : st->rp.h;
-        bp.round = FIRST ? 0u : st->rp.round + 1;
-        bp.tag = tag + 1;
-        if (!FIRST) {
-          uint32_t r = st->rp.round;
-          if (r < MAX_TRACE) {
-            st->tr_live[r] = n_live;
-            st->tr_kept[r] = tot;
-            st->tr_nseg[r] = nseg;
-          }
-          st->rp.active = 0;
-        }
-        st->bp = bp;
-        st->seq = tag + 1;
-        st->ctr_book = 0;
+      for (int j = 0; j < RITEMS; j++) {
+        if (key[j] == NOKEY) continue;
+        const uint32_t i = j * RB + tid;
+        const uint32_t s = key[j] % K;
+        const size_t e = (size_t)(lo + key[j] / K) * K + s;
+        const uint32_t pos = atomicAdd(&cursor[e], 1u);
+        const uint32_t qi = si[i];
+        atomic_max_key(&ws.slot_key[e], khi_[j], qi);
+        const size_t dst = (size_t)s * rcap + pos;
+        outx[dst] = sx[i];
+        outy[dst] = sx[RTILE + i];
+        if (DIM == 3) outz[dst] = sx[2 * RTILE + i];
+        outi[dst] = qi;
       }
     }
-    __syncthreads();
+    __syncthreads();  // stage b, window b and the child arrays are free
+  }
 
-    // ---- copy-out (coalesced per stream)
-    for (uint32_t e = tid; e < N; e += BLOCK) {
-      uint32_t s = (e >= sh_.off[1]) + (K == 3 ? (e >= sh_.off[2]) : 0);
-      size_t dst = (size_t)s * rcap + sh_.prefix[s] + (e - sh_.off[s]);
-      outx[dst] = sx[e];
-      outy[dst] = sy[e];
-      if (DIM == 3) outz[dst] = sz[e];
-      outi[dst] = sidx[e];
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    for (int s = 0; s < K; s++)
-      if (sh_.pend_valid[s]) flush_atomic(ws, sh_.pend_key[s], sh_.pend[s]);
-  }
   if (FIRST && DIM == 3) {
     // coplanarity check input: max |d| of the first split (quickhull.py:349)
 #pragma unroll
