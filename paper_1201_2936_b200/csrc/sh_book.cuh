@@ -31,6 +31,10 @@ struct BookShared {
   uint32_t wsum[ITEMS3 * WARPS * 3];
   Sum3 agg, prefix;
   int stop[4];
+  // children spanning many next-round tiles: their tile_seg entries are
+  // filled by the whole block
+  uint32_t nfill;
+  uint32_t fill_seg[TILE3], fill_t0[TILE3], fill_n[TILE3];
 };
 
 template <int DIM>
@@ -79,6 +83,7 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
     const uint32_t base = tile * TILE3;
     const bool last_tile = tile == num_tiles - 1;
 
+    if (tid == 0) sb.nfill = 0;
     RunVal v[ITEMS3];
     uint32_t cval[ITEMS3][3];
     // 3D child face (needed before the scan for the flat test)
@@ -196,7 +201,14 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       for (int q = 0; q < K; q++) cur_out[(size_t)c * K + q] = start;
       {  // first segment of every next-round tile that starts inside [start, start+cnt)
         uint32_t t0 = (start + RTILE - 1) / RTILE, t1 = (start + v[j].cnt - 1) / RTILE;
-        for (uint32_t t = t0; t <= t1; t++) tile_seg[t] = c;
+        if (t1 >= t0 + 8) {
+          uint32_t q = atomicAdd(&sb.nfill, 1u);
+          sb.fill_seg[q] = c;
+          sb.fill_t0[q] = t0;
+          sb.fill_n[q] = t1 - t0 + 1;
+        } else {
+          for (uint32_t t = t0; t <= t1; t++) tile_seg[t] = c;
+        }
       }
       double F[3];
       F[0] = ld_coord(st->px, stride, far);
@@ -249,6 +261,12 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
         }
         ch3[c] = g;
       }
+    }
+
+    __syncthreads();
+    for (uint32_t q = 0; q < sb.nfill; q++) {
+      const uint32_t c = sb.fill_seg[q], t0 = sb.fill_t0[q], nt = sb.fill_n[q];
+      for (uint32_t t = tid; t < nt; t += BLOCK) tile_seg[t0 + t] = c;
     }
 
     // ---- finalise the launch: next round's parameters + loop condition

@@ -113,8 +113,6 @@ static void free_ws(sh_ctx* c) {
   cudaFree(w.red);
   cudaFree(w.st);
   filter_free(c->fws);
-  DevState* keep = nullptr;
-  (void)keep;
   w = Workspace{};
   c->fws = FilterWs{};
   for (auto& g : c->g) {

@@ -147,6 +147,47 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   };
   const uint32_t G = gridDim.x * BLOCK;
   uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  bool aligned = stride == 1;
+#pragma unroll
+  for (int k = 0; k < DIM; k++) aligned = aligned && ((reinterpret_cast<uintptr_t>(P[k]) & 15) == 0);
+  if (aligned) {
+    // structure of arrays: 16-byte loads of point pairs, 4 pairs in flight
+    const uint32_t npair = n / 2;
+    uint32_t pi = blockIdx.x * BLOCK + threadIdx.x;
+    for (; (uint64_t)pi + 3ull * G < npair; pi += 4 * G) {
+      double2 v[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int k = 0; k < DIM; k++) v[u][k] = __ldcs(reinterpret_cast<const double2*>(P[k]) + pi + u * G);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        LexRec a, b2;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          a.c[k] = (k < DIM) ? v[u][k].x : 0.0;
+          b2.c[k] = (k < DIM) ? v[u][k].y : 0.0;
+        }
+        a.idx = 2 * (pi + u * G);
+        b2.idx = a.idx + 1;
+        a.pad = b2.pad = 0;
+        visit(a);
+        visit(b2);
+      }
+    }
+    for (; pi < npair; pi += G) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        LexRec q;
+#pragma unroll
+        for (int k = 0; k < 3; k++) q.c[k] = (k < DIM) ? ld_coord(P[k], 1, 2 * pi + h) : 0.0;
+        q.idx = 2 * pi + h;
+        q.pad = 0;
+        visit(q);
+      }
+    }
+    i = (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) ? n - 1 : n;  // odd tail
+  }
   for (; (uint64_t)i + 3ull * G < n; i += 4 * G) {  // 4 independent loads in flight
     LexRec q[4];
 #pragma unroll

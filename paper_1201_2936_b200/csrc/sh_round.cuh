@@ -32,6 +32,8 @@
 // slow path with per-point global atomics.
 #pragma once
 
+#include <type_traits>
+
 #include "sh_common.cuh"
 
 namespace sh {
@@ -58,6 +60,11 @@ struct RoundShared {
   uint32_t pend_complete[2];         // its aggregate covers it from its first point
   unsigned long long pend_hi[2][DIM];
   uint32_t pend_idx[2][DIM];
+  // uniform tiles: per-warp totals / maxima, then per-warp output bases
+  uint32_t wtot[RB / 32][DIM];
+  unsigned long long whi[RB / 32][DIM];
+  uint32_t widx[RB / 32][DIM];
+  uint32_t boff[RB / 32][DIM];
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -67,6 +74,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -152,11 +163,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   const uint32_t* segstart = ws.segstart[cur];
   const uint64_t* seg_phys = ws.seg_phys[cur];
   const uint32_t* tile_seg = ws.tile_seg[cur];
-  const Seg2* seg2 = reinterpret_cast<const Seg2*>(ws.seg[cur]);
-  const Seg3* seg3 = reinterpret_cast<const Seg3*>(ws.seg[cur]);
   uint32_t* cursor = ws.cursor[cur];
-  const uint32_t block_begin = t0 * RTILE;
-  const uint32_t block_end = min(t1 * RTILE, n_live);
 
   // first-split constants
   double f_pa[3], f_pb[3], f_nrm[3], f_thr = 0;
@@ -216,19 +223,66 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     uint32_t* si = reinterpret_cast<uint32_t*>(sx + DIM * RTILE);
     uint16_t* sw = reinterpret_cast<uint16_t*>(si + RTILE);
     const uint32_t base = t * RTILE;
+    const uint32_t cnt = min((uint32_t)RTILE, n_live - base);
     const uint32_t lo = S.wlo[b], nw = S.wn[b];
     const bool slow = S.wslow[b] != 0;
+    // a full tile inside one segment is one contiguous run of records:
+    // 16-byte copies when the run is aligned
+    const double *gx = nullptr, *gy = nullptr, *gz = nullptr;
+    const uint32_t* gi = nullptr;
+    bool contig = false;
+    if (FIRST) {
+      contig = pstride == 1;
+      gx = px + base;
+      gy = py + base;
+      gz = pz + base;
+    } else if (!slow && S.wstart[b][1] >= base + cnt) {
+      const uint64_t p0 = S.wphys[b][0] + (base - S.wstart[b][0]);
+      contig = true;
+      gx = inx + p0;
+      gy = iny + p0;
+      gz = inz + p0;
+      gi = ini + p0;
+    }
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (contig && cnt == RTILE && al16(gx) && al16(gy) && (DIM == 2 || al16(gz))) {
+#pragma unroll
+      for (int jp = 0; jp < RITEMS / 2; jp++) {
+        const uint32_t e = 2 * (jp * RB + tid);
+        cp_async16(&sx[e], gx + e);
+        cp_async16(&sx[RTILE + e], gy + e);
+        if (DIM == 3) cp_async16(&sx[2 * RTILE + e], gz + e);
+      }
+      if (!FIRST) {
+        if (al16(gi)) {
+#pragma unroll
+          for (int jq = 0; jq < RITEMS / 4; jq++) {
+            const uint32_t e = 4 * (jq * RB + tid);
+            cp_async16(&si[e], gi + e);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < RITEMS; j++) cp_async4(&si[j * RB + tid], gi + j * RB + tid);
+        }
+      }
+      cp_async_commit();
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < RITEMS; j++) {
       const uint32_t i = j * RB + tid;
       const uint32_t q = base + i;
-      if (q >= n_live) continue;
+      if (i >= cnt) continue;
       if (FIRST) {
         const int64_t o = (int64_t)q * pstride;
         cp_async8(&sx[i], px + o);
         cp_async8(&sx[RTILE + i], py + o);
         if (DIM == 3) cp_async8(&sx[2 * RTILE + i], pz + o);
-        sw[i] = 0;
+      } else if (contig) {
+        cp_async8(&sx[i], gx + i);
+        cp_async8(&sx[RTILE + i], gy + i);
+        if (DIM == 3) cp_async8(&sx[2 * RTILE + i], gz + i);
+        cp_async4(&si[i], gi + i);
       } else {
         uint32_t w;
         uint64_t phys;
@@ -286,19 +340,19 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     const uint32_t pout = lt & 1u;
 
     // ---- classify
+    const bool uniform = S.wstart[b][1] >= tile_end;  // the whole tile lies in window segment 0
     uint32_t key[RITEMS], rank[RITEMS];
     unsigned long long khi_[RITEMS];
-#pragma unroll
-    for (int j = 0; j < RITEMS; j++) {
+    auto classify_item = [&](int j, bool uni, auto&& seg_of) {
       const uint32_t i = j * RB + tid;
       const uint32_t q = tile_begin + i;
       key[j] = NOKEY;
       rank[j] = 0;
       khi_[j] = 0;
-      if (q >= tile_end) continue;
+      if (q >= tile_end) return;
       const double qx = sx[i], qy = sx[RTILE + i];
       const double qz = (DIM == 3) ? sx[2 * RTILE + i] : 0.0;
-      const uint32_t w = sw[i];
+      const uint32_t w = uni ? 0u : (uint32_t)sw[i];
       double dn = 0.0;
       int s = -1;
       if (FIRST) {
@@ -322,16 +376,160 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         }
       } else {
         const uint32_t qi = si[i];
-        if (DIM == 2) s = classify2(seg2[lo + w], qx, qy, qi, &dn);
-        else s = classify3(seg3[lo + w], qx, qy, qz, qi, &dn);
+        if constexpr (DIM == 2) s = classify2(seg_of(w), qx, qy, qi, &dn);
+        else s = classify3(seg_of(w), qx, qy, qz, qi, &dn);
       }
       if (s >= 0) {
         key[j] = w * K + (uint32_t)s;
-        khi_[j] = ordered_bits(dn);
+        // d > 0 for every live point except the 3D first split's near-plane
+        // side-0 points, so the raw bits already order correctly there
+        khi_[j] = (FIRST && DIM == 3) ? ordered_bits(dn)
+                                      : (unsigned long long)__double_as_longlong(dn) | 0x8000000000000000ull;
       }
+    };
+    using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
+    const SegT* segtab = reinterpret_cast<const SegT*>(ws.seg[cur]);
+    if (FIRST || (uniform && !slow)) {
+      SegT g0;
+      if (!FIRST) g0 = segtab[lo];  // one table load per thread per tile
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) classify_item(j, true, [&](uint32_t) -> const SegT& { return g0; });
+    } else {
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++)
+        classify_item(j, false, [&](uint32_t w) -> const SegT& { return segtab[lo + w]; });
     }
 
-    if (!slow) {
+    // close, carry or merge child (window segment w, state s) of this tile
+    auto close_child = [&](uint32_t w, uint32_t s, unsigned long long hi, uint32_t idx) {
+      const uint32_t seg = lo + w;
+      const uint32_t segbeg = S.wstart[b][w], segend = S.wstart[b][w + 1];
+      bool complete = segbeg >= tile_begin;
+      if (w == 0 && S.pend_seg[pin] == seg) {
+        const unsigned long long ph = S.pend_hi[pin][s];
+        const uint32_t pi = S.pend_idx[pin][s];
+        if (ph > hi || (ph == hi && pi < idx)) {
+          hi = ph;
+          idx = pi;
+        }
+        complete = S.pend_complete[pin] != 0;
+      }
+      const bool continues = segend > tile_end;
+      if (continues && has_next && w == nw - 1) {
+        S.pend_hi[pout][s] = hi;
+        S.pend_idx[pout][s] = idx;
+        if (s == 0) {
+          S.pend_seg[pout] = seg;
+          S.pend_complete[pout] = complete ? 1u : 0u;
+        }
+      } else if (hi) {
+        Key128* slot = &ws.slot_key[(size_t)seg * K + s];
+        if (complete && !continues) {
+          Key128 kv;
+          kv.hi = hi;
+          kv.lo = idx;
+          st_cg(slot, kv);
+        } else {
+          atomic_max_key(slot, hi, idx);
+        }
+      }
+    };
+    const int warp = tid >> 5;
+
+    if (!slow && uniform) {
+      // ---- one segment: ballots for ranks, register maxima, one claim per state
+      uint32_t wrun[K];
+      unsigned long long hm[K];
+      uint32_t im[K];
+#pragma unroll
+      for (int s = 0; s < K; s++) {
+        wrun[s] = 0;
+        hm[s] = 0ull;
+        im[s] = 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) {
+        uint32_t r = 0;
+#pragma unroll
+        for (int s = 0; s < K; s++) {
+          const bool mine = key[j] == (uint32_t)s;
+          const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+          r = mine ? wrun[s] + __popc(m & lanemask_lt()) : r;
+          wrun[s] += __popc(m);
+          const unsigned long long v = mine ? khi_[j] : 0ull;
+          hm[s] = v > hm[s] ? v : hm[s];
+        }
+        rank[j] = r;
+      }
+#pragma unroll
+      for (int s = 0; s < K; s++) {
+        const uint32_t mu = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)(hm[s] >> 32));
+        const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, ((uint32_t)(hm[s] >> 32) == mu) ? (uint32_t)hm[s] : 0u);
+        hm[s] = ((unsigned long long)mu << 32) | ml;
+      }
+      // lowest original index among the warp's farthest points
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) {
+        const uint32_t i = j * RB + tid;
+        const uint32_t qi = FIRST ? tile_begin + i : si[i];
+#pragma unroll
+        for (int s = 0; s < K; s++) {
+          const uint32_t c = (key[j] == (uint32_t)s && khi_[j] == hm[s]) ? qi : 0xFFFFFFFFu;
+          im[s] = c < im[s] ? c : im[s];
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < K; s++) {
+        im[s] = __reduce_min_sync(0xFFFFFFFFu, im[s]);
+        if (lane == 0) {
+          S.wtot[warp][s] = wrun[s];
+          S.whi[warp][s] = hm[s];
+          S.widx[warp][s] = im[s];
+        }
+      }
+      __syncthreads();
+      if (tid < K) {
+        const uint32_t s = tid;
+        uint32_t tot = 0;
+        unsigned long long hi = 0ull;
+        uint32_t idx = 0xFFFFFFFFu;
+#pragma unroll
+        for (int w = 0; w < RB / 32; w++) {
+          tot += S.wtot[w][s];
+          const unsigned long long h2 = S.whi[w][s];
+          const uint32_t i2 = S.widx[w][s];
+          if (h2 > hi || (h2 == hi && i2 < idx)) {
+            hi = h2;
+            idx = i2;
+          }
+        }
+        uint32_t base = tot ? atomicAdd(&cursor[(size_t)lo * K + s], tot) : 0u;
+#pragma unroll
+        for (int w = 0; w < RB / 32; w++) {
+          S.boff[w][s] = base;
+          base += S.wtot[w][s];
+        }
+        close_child(0, s, hi, idx);
+      }
+      __syncthreads();
+      size_t wb[K];
+#pragma unroll
+      for (int s = 0; s < K; s++) wb[s] = (size_t)s * rcap + S.boff[warp][s];
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++) {
+        if (key[j] == NOKEY) continue;
+        const uint32_t i = j * RB + tid;
+        size_t dst = wb[0];
+#pragma unroll
+        for (int s = 1; s < K; s++) dst = key[j] == (uint32_t)s ? wb[s] : dst;
+        dst += rank[j];
+        outx[dst] = sx[i];
+        outy[dst] = sx[RTILE + i];
+        if (DIM == 3) outz[dst] = sx[2 * RTILE + i];
+        outi[dst] = FIRST ? (tile_begin + i) : si[i];
+      }
+      if (tid == 0 && !(has_next && S.wstart[b][nw] > tile_end)) S.pend_seg[pout] = NOKEY;
+    } else if (!slow) {
       // ---- per (segment, state): tile-local ranks, counts, farthest keys
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
@@ -400,40 +598,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       }
       // ---- close, carry or merge every child of the tile
       for (uint32_t e = tid; e < ne; e += RB) {
-        const uint32_t w = e / K, s = e % K;
-        const uint32_t seg = lo + w;
-        const uint32_t segbeg = S.wstart[b][w], segend = S.wstart[b][w + 1];
-        unsigned long long hi = S.kcnt[e] ? S.khi[e] : 0ull;
-        uint32_t idx = S.kidx[e];
-        bool complete = segbeg >= tile_begin;
-        if (w == 0 && S.pend_seg[pin] == seg) {
-          const unsigned long long ph = S.pend_hi[pin][s];
-          const uint32_t pi = S.pend_idx[pin][s];
-          if (ph > hi || (ph == hi && pi < idx)) {
-            hi = ph;
-            idx = pi;
-          }
-          complete = S.pend_complete[pin] != 0;
-        }
-        const bool continues = segend > tile_end;
-        if (continues && has_next && w == nw - 1) {
-          S.pend_hi[pout][s] = hi;
-          S.pend_idx[pout][s] = idx;
-          if (s == 0) {
-            S.pend_seg[pout] = seg;
-            S.pend_complete[pout] = complete ? 1u : 0u;
-          }
-        } else if (hi) {
-          Key128* slot = &ws.slot_key[(size_t)seg * K + s];
-          if (complete && !continues) {
-            Key128 kv;
-            kv.hi = hi;
-            kv.lo = idx;
-            st_cg(slot, kv);
-          } else {
-            atomic_max_key(slot, hi, idx);
-          }
-        }
+        close_child(e / K, e % K, S.kcnt[e] ? S.khi[e] : 0ull, S.kidx[e]);
         S.kcnt[e] = 0;
         S.khi[e] = 0ull;
         S.kidx[e] = 0xFFFFFFFFu;
