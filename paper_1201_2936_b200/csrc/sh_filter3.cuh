@@ -10,10 +10,13 @@
 //
 //   F0 k_f_setup    grid size from the candidate count m, reset the cells
 //   F1 k_f_gather   candidate coordinates (discovery order) + bbox
-//   F2 k_f_count    uniform G^3 grid (G = 4..64, ~4 candidates per cell):
-//                   cell of each candidate, tight cell / superblock boxes
+//   F2 k_f_count    uniform G^3 grid (G a power of two <= 64, ~1 candidate
+//                   per cell) numbered in Morton order
 //   F3 k_f_scan     cell offsets (one block)
-//   F4 k_f_scatter  candidates sorted by cell
+//   F4 k_f_scatter  candidates sorted by cell, i.e. along a Morton curve
+//   F4b k_f_boxes   a 32-ary box tree over the sorted candidates: level 0 =
+//                   32 consecutive candidates, level l+1 = 32 level-l nodes,
+//                   tight fp64 boxes
 //   F5 k_f_test     one warp per candidate:
 //                     (1) certificate: no other candidate above the plane
 //                         through v with normal v - bbox centre (+eps) -> keep
@@ -23,11 +26,11 @@
 //                         every face farther than eps -> prune; anything
 //                         closer than eps -> keep (the reference's
 //                         eps-tolerant supporting plane keeps it too).
-//                   Both use a branch-and-bound support query over the
-//                   grid: a box is skipped when the monotone fp64 upper
-//                   bound of d.(c - v) over it can not beat the best value
-//                   (IEEE rounding is monotone, so the bound computed with
-//                   the point formula's operation order is exact).
+//                   Both use a best-first branch-and-bound support query
+//                   down the tree: a node is skipped when the fp64 upper
+//                   bound of d.(c - v) over its box can not beat the best
+//                   value (IEEE rounding is monotone, so the bound computed
+//                   with the point formula's operation order is exact).
 //   F6 k_f_compact  kept candidates -> user indices, discovery order kept
 //                   (verts[extreme], quickhull.py:311)
 // m <= 4 keeps everything (quickhull.py:148-149).
@@ -38,15 +41,22 @@
 namespace sh {
 
 constexpr uint32_t ST_CAND_OVERFLOW = 7;
-constexpr int FG_MAX = 64;   // grid cells per axis (max)
-constexpr int FSB = 4;       // cells per superblock per axis
-constexpr int F_TEST_BLOCK = 256;
+constexpr int FG_MAX = 64;   // grid cells per axis (max, power of two)
+constexpr int F_LEVELS = 6;  // box-tree levels: 32^6 candidates max
+constexpr int F_TEST_BLOCK = 128;
+constexpr int F_STACK = 32 * F_LEVELS;  // traversal stack entries per warp
+#ifndef F_PER_CELL
+#define F_PER_CELL 1.0   // target candidates per grid cell
+#endif
 
 struct FilterParams {
-  uint32_t m, G, GS, ctr_test;
+  uint32_t m, G, nlev, ctr_test;
+  uint32_t lnodes[F_LEVELS];   // nodes per tree level
+  uint32_t loff[F_LEVELS];     // first node of each level in nbox
   double lo[3], inv_h[3], ctr[3];
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
   uint32_t ambiguous, gjk_capped, pad0, pad1;
+  unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
 };
 
 struct FilterWs {
@@ -60,8 +70,7 @@ struct FilterWs {
   double *sx, *sy, *sz;              // candidates sorted by cell
   uint32_t* sid;                     // discovery index of sorted entry
   uint32_t *cell_cnt, *cell_start, *cell_cur;
-  unsigned long long* cell_box;      // [cell][6] ordered bits
-  unsigned long long* sb_box;        // [superblock][6]
+  double* nbox;                      // [node][6]: lo x,y,z, hi x,y,z (all levels)
   uint8_t* keep;
 };
 
@@ -69,7 +78,7 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
   bool ok = true;
   auto A = [&](void** p, size_t b) { ok &= cudaMalloc(p, b + 64) == cudaSuccess; };
   const size_t cells = (size_t)FG_MAX * FG_MAX * FG_MAX;
-  const size_t sbs = cells / (FSB * FSB * FSB);
+  const size_t nodes = mcap / 31 + 2 * F_LEVELS + 8;
   A((void**)&f.result, 64);
   A((void**)&f.fp, sizeof(FilterParams));
   A((void**)&f.cx, mcap * 8);
@@ -84,15 +93,14 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
   A((void**)&f.cell_cnt, cells * 4);
   A((void**)&f.cell_start, (cells + 1) * 4);
   A((void**)&f.cell_cur, cells * 4);
-  A((void**)&f.cell_box, cells * 48);
-  A((void**)&f.sb_box, sbs * 48);
+  A((void**)&f.nbox, nodes * 48);
   f.mcap = (uint32_t)mcap;
   return ok ? 0 : 1;
 }
 
 static inline void filter_free(FilterWs& f) {
   void* ps[] = {f.result, f.fp, f.cx, f.cy, f.cz, f.sx, f.sy, f.sz, f.ccell, f.sid, f.keep,
-                f.cell_cnt, f.cell_start, f.cell_cur, f.cell_box, f.sb_box};
+                f.cell_cnt, f.cell_start, f.cell_cur, f.nbox};
   for (void* p : ps)
     if (p) cudaFree(p);
   int32_t* of = f.out_facets;
@@ -109,14 +117,27 @@ static inline int filter_set_params(FilterWs& f, int32_t* facets, int64_t cap, c
   return 0;
 }
 
+// per-warp diagnostics (every lane holds the same values)
+struct FStat {
+  unsigned long long scanned, queries, iters, certified;
+};
+
 __device__ __forceinline__ unsigned long long obits(double d) { return ordered_bits(d); }
 __device__ __forceinline__ double ofrom(unsigned long long b) { return from_ordered_bits(b); }
 
 __device__ __forceinline__ uint32_t f_grid_of(uint32_t m) {
-  // ~4 candidates per cell, G a multiple of the superblock edge
-  double g = cbrt((double)m / 4.0);
-  uint32_t G = (uint32_t)(FSB * ceil(g / FSB));
-  return G < FSB ? FSB : (G > FG_MAX ? FG_MAX : G);
+  // ~F_PER_CELL candidates per cell, G a power of two
+  double g = cbrt((double)m / F_PER_CELL);
+  uint32_t G = 2;
+  while (G < FG_MAX && (double)G < g) G <<= 1;
+  return G;
+}
+
+__device__ __forceinline__ uint32_t spread3(uint32_t x) {  // 6 bits -> every third bit
+  uint32_t r = 0;
+#pragma unroll
+  for (int b = 0; b < 6; b++) r |= ((x >> b) & 1u) << (3 * b);
+  return r;
 }
 
 // ------------------------------------------------------------------ F0
@@ -124,32 +145,31 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
   DevState* st = ws.st;
   uint32_t m = st->h_final;
   if (m > f.mcap) m = 0;  // overflow: reported below, nothing else runs
-  const uint32_t G = f_grid_of(m), GS = G / FSB;
-  const uint32_t cells = G * G * G, sbs = GS * GS * GS;
+  const uint32_t G = f_grid_of(m);
+  const uint32_t cells = G * G * G;
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
-  for (uint32_t c = tid; c < cells; c += T) {
-    f.cell_cnt[c] = 0;
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      f.cell_box[(size_t)c * 6 + k] = ~0ull;
-      f.cell_box[(size_t)c * 6 + 3 + k] = 0ull;
-    }
-  }
-  for (uint32_t c = tid; c < sbs; c += T) {
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      f.sb_box[(size_t)c * 6 + k] = ~0ull;
-      f.sb_box[(size_t)c * 6 + 3 + k] = 0ull;
-    }
-  }
+  for (uint32_t c = tid; c < cells; c += T) f.cell_cnt[c] = 0;
   if (tid == 0) {
     FilterParams* P = f.fp;
     P->m = m;
     P->G = G;
-    P->GS = GS;
     P->ctr_test = 0;
     P->ambiguous = 0;
     P->gjk_capped = 0;
+    P->queries = 0;
+    P->scanned = 0;
+    P->gjk_iters = 0;
+    P->certified = 0;
+    // box tree: level 0 = chunks of 32 candidates, level l+1 = 32 level-l nodes
+    uint32_t nl = m ? (m + 31) / 32 : 0, off = 0, lev = 0;
+    for (int l = 0; l < F_LEVELS; l++) {
+      P->lnodes[l] = nl;
+      P->loff[l] = off;
+      if (nl) lev = l + 1;
+      off += nl;
+      nl = (nl <= 1) ? 0 : (nl + 31) / 32;
+    }
+    P->nlev = lev;
     for (int k = 0; k < 3; k++) {
       P->bb[k] = ~0ull;
       P->bb[3 + k] = 0ull;
@@ -202,13 +222,12 @@ __global__ void __launch_bounds__(BLOCK) k_f_gather(Workspace ws, FilterWs f) {
 // ------------------------------------------------------------------ F2
 struct GridGeom {
   double lo[3], inv_h[3];
-  uint32_t G, GS;
+  uint32_t G;
 };
 
 __device__ __forceinline__ GridGeom f_geom(const FilterParams* P) {
   GridGeom g;
   g.G = P->G;
-  g.GS = P->GS;
 #pragma unroll
   for (int k = 0; k < 3; k++) {
     double lo = ofrom(P->bb[k]), hi = ofrom(P->bb[3 + k]);
@@ -237,22 +256,10 @@ __global__ void __launch_bounds__(BLOCK) k_f_count(Workspace ws, FilterWs f) {
     }
   }
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    double c[3] = {f.cx[i], f.cy[i], f.cz[i]};
-    uint32_t a[3];
-#pragma unroll
-    for (int k = 0; k < 3; k++) a[k] = f_axis_cell(g, k, c[k]);
-    uint32_t cell = (a[2] * g.G + a[1]) * g.G + a[0];
-    uint32_t sb = ((a[2] / FSB) * g.GS + a[1] / FSB) * g.GS + a[0] / FSB;
+    const uint32_t cell = spread3(f_axis_cell(g, 0, f.cx[i])) | (spread3(f_axis_cell(g, 1, f.cy[i])) << 1) |
+                          (spread3(f_axis_cell(g, 2, f.cz[i])) << 2);
     f.ccell[i] = cell;
     atomicAdd(&f.cell_cnt[cell], 1u);
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      unsigned long long b = obits(c[k]);
-      atomicMin(&f.cell_box[(size_t)cell * 6 + k], b);
-      atomicMax(&f.cell_box[(size_t)cell * 6 + 3 + k], b);
-      atomicMin(&f.sb_box[(size_t)sb * 6 + k], b);
-      atomicMax(&f.sb_box[(size_t)sb * 6 + 3 + k], b);
-    }
   }
 }
 
@@ -308,6 +315,97 @@ __global__ void __launch_bounds__(BLOCK) k_f_scatter(FilterWs f) {
   }
 }
 
+// ------------------------------------------------------------------ F4b
+// levels 0 and 1: a block of 32 warps builds 32 level-0 boxes (one warp
+// per 32 sorted candidates) and the level-1 box above them
+__global__ void __launch_bounds__(1024) k_f_boxes01(FilterWs f) {
+  __shared__ double sbx[32][6];
+  const FilterParams* P = f.fp;
+  const uint32_t m = P->m, n0 = P->lnodes[0], n1 = P->lnodes[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t base = blockIdx.x * 32; base < n0; base += gridDim.x * 32) {
+    const uint32_t node = base + warp;
+    double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    const uint32_t p = node * 32 + lane;
+    if (node < n0 && p < m) {
+      const double c[3] = {f.sx[p], f.sy[p], f.sz[p]};
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        b[k] = c[k];
+        b[3 + k] = c[k];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        b[k] = fmin(b[k], __shfl_xor_sync(0xFFFFFFFFu, b[k], o));
+        b[3 + k] = fmax(b[3 + k], __shfl_xor_sync(0xFFFFFFFFu, b[3 + k], o));
+      }
+    }
+    if (lane < 6) {
+      double v = b[0];
+#pragma unroll
+      for (int k = 1; k < 6; k++) v = (lane == k) ? b[k] : v;
+      sbx[warp][lane] = v;
+      if (node < n0) f.nbox[(size_t)(P->loff[0] + node) * 6 + lane] = v;
+    }
+    __syncthreads();
+    if (warp == 0 && n1 > 0) {
+      double c[6];
+#pragma unroll
+      for (int k = 0; k < 6; k++) c[k] = sbx[lane][k];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          c[k] = fmin(c[k], __shfl_xor_sync(0xFFFFFFFFu, c[k], o));
+          c[3 + k] = fmax(c[3 + k], __shfl_xor_sync(0xFFFFFFFFu, c[3 + k], o));
+        }
+      }
+      if (lane < 6) {
+        double v = c[0];
+#pragma unroll
+        for (int k = 1; k < 6; k++) v = (lane == k) ? c[k] : v;
+        f.nbox[(size_t)(P->loff[1] + base / 32) * 6 + lane] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// levels 2.. (at most a few hundred nodes): one block, one warp per node
+__global__ void __launch_bounds__(1024) k_f_boxes_hi(FilterWs f) {
+  const FilterParams* P = f.fp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = 2; l < (int)P->nlev; l++) {
+    const uint32_t nl = P->lnodes[l], nc = P->lnodes[l - 1];
+    for (uint32_t node = warp; node < nl; node += 32) {
+      double c[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      const uint32_t ch = node * 32 + lane;
+      if (ch < nc) {
+#pragma unroll
+        for (int k = 0; k < 6; k++) c[k] = f.nbox[(size_t)(P->loff[l - 1] + ch) * 6 + k];
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          c[k] = fmin(c[k], __shfl_xor_sync(0xFFFFFFFFu, c[k], o));
+          c[3 + k] = fmax(c[3 + k], __shfl_xor_sync(0xFFFFFFFFu, c[3 + k], o));
+        }
+      }
+      if (lane < 6) {
+        double v = c[0];
+#pragma unroll
+        for (int k = 1; k < 6; k++) v = (lane == k) ? c[k] : v;
+        f.nbox[(size_t)(P->loff[l] + node) * 6 + lane] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ F5
 struct V3 {
   double x, y, z;
@@ -327,12 +425,10 @@ __device__ __forceinline__ V3 vcross(V3 u, V3 v) {
 __device__ __forceinline__ V3 vneg(V3 a) { return v3(-a.x, -a.y, -a.z); }
 
 // max over the box of d.(c - v), evaluated with the point formula's order
-__device__ __forceinline__ double box_bound(const unsigned long long* b, V3 d, V3 v) {
-  double lo0 = ofrom(b[0]), lo1 = ofrom(b[1]), lo2 = ofrom(b[2]);
-  double hi0 = ofrom(b[3]), hi1 = ofrom(b[4]), hi2 = ofrom(b[5]);
-  double t0 = fmax(mul(d.x, sub(lo0, v.x)), mul(d.x, sub(hi0, v.x)));
-  double t1 = fmax(mul(d.y, sub(lo1, v.y)), mul(d.y, sub(hi1, v.y)));
-  double t2 = fmax(mul(d.z, sub(lo2, v.z)), mul(d.z, sub(hi2, v.z)));
+__device__ __forceinline__ double box_bound(const double* b, V3 d, V3 v) {
+  const double t0 = fmax(mul(d.x, sub(__ldg(b + 0), v.x)), mul(d.x, sub(__ldg(b + 3), v.x)));
+  const double t1 = fmax(mul(d.y, sub(__ldg(b + 1), v.y)), mul(d.y, sub(__ldg(b + 4), v.y)));
+  const double t2 = fmax(mul(d.z, sub(__ldg(b + 2), v.z)), mul(d.z, sub(__ldg(b + 5), v.z)));
   return add(add(t0, t1), t2);
 }
 
@@ -350,115 +446,107 @@ __device__ __forceinline__ void sup_merge(Sup& a, double val, uint32_t pos, uint
   }
 }
 
-// Scan the points of one cell (warp-cooperative), updating `best`.
-// first_hit: stop at the first value > thr (existence query).
-__device__ __forceinline__ bool scan_cell(const FilterWs& f, uint32_t cell, V3 d, V3 v, uint32_t self,
-                                          double thr, bool first_hit, Sup& best) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t s0 = f.cell_start[cell], s1 = f.cell_start[cell + 1];
-  for (uint32_t p0 = s0; p0 < s1; p0 += 32) {
-    uint32_t p = p0 + lane;
-    double val = -INFINITY;
-    uint32_t id = 0xFFFFFFFFu;
-    if (p < s1) {
-      id = f.sid[p];
-      if (id != self) {
-        V3 c = v3(f.sx[p], f.sy[p], f.sz[p]);
-        val = vdot(d, vsub(c, v));
-      }
-    }
-    Sup s;
-    s.val = val;
-    s.pos = p;
-    s.id = id;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      double ov = __shfl_xor_sync(0xFFFFFFFFu, s.val, o);
-      uint32_t op = __shfl_xor_sync(0xFFFFFFFFu, s.pos, o);
-      uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, s.id, o);
-      sup_merge(s, ov, op, oi);
-    }
-    sup_merge(best, s.val, s.pos, s.id);
-    if (first_hit && best.val > thr) return true;
-  }
-  return false;
-}
+struct FStack {
+  uint32_t node[F_STACK];  // (level << 26) | node
+  double bound[F_STACK];
+};
 
-__device__ __forceinline__ bool scan_superblock(const FilterWs& f, const GridGeom& g, uint32_t sb, V3 d,
-                                                V3 v, uint32_t self, double thr, bool first_hit,
-                                                Sup& best) {
+// Best-first branch-and-bound support query down the box tree:
+// max over candidates c != self of d.(c - v).  first_hit: stop at the first
+// value > thr (existence query).  Warp-cooperative; every lane returns the
+// same result.
+__device__ Sup support_query(const FilterWs& f, const FilterParams& P, V3 d, V3 v, uint32_t self,
+                             double thr, bool first_hit, FStack& stk, FStat& fs) {
   const int lane = threadIdx.x & 31;
-  const uint32_t GS = g.GS, G = g.G;
-  const uint32_t bx = sb % GS, by = (sb / GS) % GS, bz = sb / (GS * GS);
-#pragma unroll 1
-  for (int half = 0; half < 2; half++) {
-    const uint32_t l = half * 32 + lane;  // 64 cells per superblock
-    const uint32_t cell = ((bz * FSB + l / 16) * G + (by * FSB + (l / 4) % 4)) * G + bx * FSB + l % 4;
-    double bnd = -INFINITY;
-    if (f.cell_box[(size_t)cell * 6] != ~0ull) bnd = box_bound(&f.cell_box[(size_t)cell * 6], d, v);
-    const double floor_ = first_hit ? thr : best.val;
-    uint32_t mask = __ballot_sync(0xFFFFFFFFu, bnd > floor_ || (!first_hit && bnd == floor_ && bnd > -INFINITY));
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const double cb = __shfl_sync(0xFFFFFFFFu, bnd, src);
-      const uint32_t cc = __shfl_sync(0xFFFFFFFFu, cell, src);
-      if (!first_hit && cb < best.val) continue;
-      if (scan_cell(f, cc, d, v, self, thr, first_hit, best)) return true;
-    }
-  }
-  return false;
-}
-
-// Branch-and-bound support query: max over candidates c != self of d.(c-v).
-__device__ Sup support_query(const FilterWs& f, const GridGeom& g, V3 d, V3 v, uint32_t self, double thr,
-                             bool first_hit) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t nsb = g.GS * g.GS * g.GS;
+  fs.queries++;
   Sup best;
   best.val = -INFINITY;
   best.pos = 0xFFFFFFFFu;
   best.id = 0xFFFFFFFFu;
-  // pass 1: the superblock with the largest bound first (tightens `best`)
-  double mb = -INFINITY;
-  uint32_t msb = 0xFFFFFFFFu;
-  for (uint32_t s0 = 0; s0 < nsb; s0 += 32) {
-    uint32_t sb = s0 + lane;
-    double b = -INFINITY;
-    if (sb < nsb && f.sb_box[(size_t)sb * 6] != ~0ull) b = box_bound(&f.sb_box[(size_t)sb * 6], d, v);
-    if (b > mb) {
-      mb = b;
-      msb = sb;
+  if (P.nlev == 0) return best;
+  int top = 0;
+  uint32_t cl = P.nlev - 1, cn = 0;  // current node: level, index
+  double cb = INFINITY;
+  bool have = true;
+  for (;;) {
+    if (!have) {
+      if (top == 0) break;
+      top--;
+      const uint32_t e = stk.node[top];
+      cl = e >> 26;
+      cn = e & ((1u << 26) - 1);
+      cb = stk.bound[top];
     }
-  }
+    have = false;
+    if (first_hit ? !(cb > thr) : (cb < best.val)) continue;
+    if (cl == 0) {
+      // leaf: 32 consecutive candidates
+      const uint32_t p = cn * 32 + lane;
+      double val = -INFINITY;
+      uint32_t id = 0xFFFFFFFFu;
+      if (p < P.m) {
+        id = __ldg(&f.sid[p]);
+        if (id != self) val = vdot(d, vsub(v3(__ldg(&f.sx[p]), __ldg(&f.sy[p]), __ldg(&f.sz[p])), v));
+      }
+      fs.scanned += 32;
+      if (first_hit) {
+        const uint32_t hit = __ballot_sync(0xFFFFFFFFu, val > thr);
+        if (hit) {
+          const int src = __ffs(hit) - 1;
+          best.val = __shfl_sync(0xFFFFFFFFu, val, src);
+          best.pos = __shfl_sync(0xFFFFFFFFu, p, src);
+          best.id = __shfl_sync(0xFFFFFFFFu, id, src);
+          return best;
+        }
+        continue;
+      }
+      if (!__ballot_sync(0xFFFFFFFFu, val >= best.val && val > -INFINITY)) continue;
+      Sup sp;
+      sp.val = val;
+      sp.pos = p;
+      sp.id = id;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    double ob = __shfl_xor_sync(0xFFFFFFFFu, mb, o);
-    uint32_t os = __shfl_xor_sync(0xFFFFFFFFu, msb, o);
-    if (ob > mb || (ob == mb && os < msb)) {
-      mb = ob;
-      msb = os;
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, sp.val, o);
+        const uint32_t op = __shfl_xor_sync(0xFFFFFFFFu, sp.pos, o);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, sp.id, o);
+        sup_merge(sp, ov, op, oi);
+      }
+      sup_merge(best, sp.val, sp.pos, sp.id);
+      continue;
     }
-  }
-  if (msb == 0xFFFFFFFFu) return best;
-  if (first_hit && !(mb > thr)) return best;
-  if (scan_superblock(f, g, msb, d, v, self, thr, first_hit, best)) return best;
-  // pass 2: every other superblock that can still win
-  for (uint32_t s0 = 0; s0 < nsb; s0 += 32) {
-    uint32_t sb = s0 + lane;
+    // inner node: bounds of its (up to) 32 children at level cl - 1
+    const uint32_t chl = cl - 1;
+    const uint32_t ch = cn * 32 + lane;
     double b = -INFINITY;
-    if (sb < nsb && sb != msb && f.sb_box[(size_t)sb * 6] != ~0ull)
-      b = box_bound(&f.sb_box[(size_t)sb * 6], d, v);
-    const double floor_ = first_hit ? thr : best.val;
-    uint32_t mask = __ballot_sync(0xFFFFFFFFu, b > floor_ || (!first_hit && b == floor_ && b > -INFINITY));
-    while (mask) {
-      const int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const double bb = __shfl_sync(0xFFFFFFFFu, b, src);
-      const uint32_t ss = s0 + src;
-      if (!first_hit && bb < best.val) continue;
-      if (scan_superblock(f, g, ss, d, v, self, thr, first_hit, best)) return best;
+    if (ch < P.lnodes[chl]) b = box_bound(f.nbox + (size_t)(P.loff[chl] + ch) * 6, d, v);
+    const bool pass = first_hit ? (b > thr) : (b >= best.val && b > -INFINITY);
+    uint32_t mask = __ballot_sync(0xFFFFFFFFu, pass);
+    if (!mask) continue;
+    // descend into the child with the largest bound, push the others
+    double mb = pass ? b : -INFINITY;
+    int ml = lane;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xFFFFFFFFu, mb, o);
+      const int oln = __shfl_xor_sync(0xFFFFFFFFu, ml, o);
+      if (ob > mb || (ob == mb && oln < ml)) {
+        mb = ob;
+        ml = oln;
+      }
     }
+    mask &= ~(1u << ml);
+    const uint32_t r = __popc(mask & lanemask_lt());
+    if (((mask >> lane) & 1u) && top + (int)r < F_STACK) {
+      stk.node[top + r] = (chl << 26) | ch;
+      stk.bound[top + r] = b;
+    }
+    top = min(top + __popc(mask), F_STACK);
+    __syncwarp();
+    cl = chl;
+    cn = cn * 32 + ml;
+    cb = mb;
+    have = true;
   }
   return best;
 }
@@ -604,8 +692,8 @@ __device__ __forceinline__ double tet_depth(const V3* W) {
 
 // 1 keep, 0 prune; *amb set when kept only because v is within eps of the
 // boundary of the other candidates' hull (or the iteration cap was hit).
-__device__ int f_decide(const FilterWs& f, const GridGeom& g, uint32_t i, V3 v, V3 ctr, double eps,
-                        int* amb, int* capped) {
+__device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t i, V3 v, V3 ctr, double eps,
+                        int* amb, int* capped, FStack& stk, FStat& fs) {
   V3 w0 = vsub(v, ctr);
   double wl = sqrt_(vdot(w0, w0));
   if (!(wl > 0.0)) {
@@ -614,8 +702,11 @@ __device__ int f_decide(const FilterWs& f, const GridGeom& g, uint32_t i, V3 v, 
   }
   // (1) certificate along v - centre
   const double thr0 = mul(eps, wl);
-  Sup s = support_query(f, g, w0, v, i, thr0, true);
-  if (!(s.val > thr0)) return 1;
+  Sup s = support_query(f, P, w0, v, i, thr0, true, stk, fs);
+  if (!(s.val > thr0)) {
+    fs.certified++;
+    return 1;
+  }
   // (2) GJK on U = {c - v : c != v}
   V3 W[4];
   uint32_t id[4];
@@ -631,7 +722,8 @@ __device__ int f_decide(const FilterWs& f, const GridGeom& g, uint32_t i, V3 v, 
       return 1;
     }
     V3 dir = vneg(x);
-    Sup q = support_query(f, g, dir, v, i, 0.0, false);
+    fs.iters++;
+    Sup q = support_query(f, P, dir, v, i, 0.0, false, stk, fs);
     if (q.pos == 0xFFFFFFFFu) return 1;
     // q.val = max_u (-x).u ; gap = x.x - min_u x.u = xx + q.val
     if (add(xx, q.val) <= 1e-13 * xx) return 1;  // origin outside: v is extreme
@@ -665,21 +757,29 @@ __device__ int f_decide(const FilterWs& f, const GridGeom& g, uint32_t i, V3 v, 
   return 1;
 }
 
-__global__ void __launch_bounds__(F_TEST_BLOCK) k_f_test(Workspace ws, FilterWs f) {
-  const FilterParams* P = f.fp;
-  const uint32_t m = P->m;
+__global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_test(Workspace ws, FilterWs f) {
+  __shared__ FilterParams sP;
+  __shared__ FStack s_stk[F_TEST_BLOCK / 32];
+  if (threadIdx.x == 0) sP = *f.fp;
+  __syncthreads();
+  const FilterParams& P = sP;
+  const uint32_t m = P.m;
   const double eps = ws.st->eps;
-  const GridGeom g = f_geom(P);
-  const V3 ctr = v3(P->ctr[0], P->ctr[1], P->ctr[2]);
+  const V3 ctr = v3(P.ctr[0], P.ctr[1], P.ctr[2]);
   const int lane = threadIdx.x & 31;
+  FStack& stk = s_stk[threadIdx.x >> 5];
   int amb_count = 0, cap_count = 0;
+  FStat fs = {0, 0, 0, 0};
   for (;;) {
-    uint32_t i = 0;
-    if (lane == 0) i = atomicAdd(&f.fp->ctr_test, 1u);
-    i = __shfl_sync(0xFFFFFFFFu, i, 0);
-    if (i >= m) break;
+    // candidates in Morton order: warps of a block work on nearby candidates
+    // and share the tree nodes they touch in L1
+    uint32_t ps = 0;
+    if (lane == 0) ps = atomicAdd(&f.fp->ctr_test, 1u);
+    ps = __shfl_sync(0xFFFFFFFFu, ps, 0);
+    if (ps >= m) break;
+    const uint32_t i = __ldg(&f.sid[ps]);
     int keep = 1, amb = 0, capped = 0;
-    if (m > 4) keep = f_decide(f, g, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, eps, &amb, &capped);
+    if (m > 4) keep = f_decide(f, P, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, eps, &amb, &capped, stk, fs);
     if (lane == 0) {
       f.keep[i] = (uint8_t)keep;
       amb_count += amb;
@@ -688,6 +788,12 @@ __global__ void __launch_bounds__(F_TEST_BLOCK) k_f_test(Workspace ws, FilterWs 
   }
   if (lane == 0 && amb_count) atomicAdd(&f.fp->ambiguous, (uint32_t)amb_count);
   if (lane == 0 && cap_count) atomicAdd(&f.fp->gjk_capped, (uint32_t)cap_count);
+  if (lane == 0 && fs.queries) {
+    atomicAdd(&f.fp->queries, fs.queries);
+    atomicAdd(&f.fp->scanned, fs.scanned);
+    atomicAdd(&f.fp->gjk_iters, fs.iters);
+    atomicAdd(&f.fp->certified, fs.certified);
+  }
 }
 
 // ------------------------------------------------------------------ F6
@@ -735,6 +841,8 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_count<<<grid, BLOCK, 0, s>>>(ws, f);
   k_f_scan<<<1, 1024, 0, s>>>(f);
   k_f_scatter<<<grid, BLOCK, 0, s>>>(f);
+  k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(f);
+  k_f_boxes_hi<<<1, 1024, 0, s>>>(f);
   k_f_test<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_compact<<<1, 1024, 0, s>>>(ws, f);
   return cudaGetLastError() == cudaSuccess ? 0 : 10;

@@ -54,10 +54,10 @@ struct sh_ctx {
   int round_occ2 = 0, round_occ3 = 0, book_occ = 0;
   uint32_t last_n = 0;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
-  // per-launch CUDA events (launch_mode 2): ev[0] before the first launch,
-  // ev[i+1] after launch i, whose kernel is prof_kind[i]
-  static constexpr int PROF_CAP = 8192;
-  cudaEvent_t ev[PROF_CAP + 1] = {};
+  // per-launch CUDA events (launch_mode 2): ev0[i] / ev1[i] right before /
+  // after launch i, whose kernel is prof_kind[i]
+  static constexpr int PROF_CAP = 4096;
+  cudaEvent_t ev0[PROF_CAP] = {}, ev1[PROF_CAP] = {};
   int prof_kind[PROF_CAP] = {};
   int prof_n = 0;
   bool prof_on = false;
@@ -67,11 +67,17 @@ struct sh_ctx {
 enum { KID_INIT = 0, KID_FIRST_REDUCE, KID_LINE_FAR, KID_ROUND_FIRST, KID_ROUND, KID_BOOK,
        KID_FILTER, KID_OUTPUT };
 
+// launch mode 2: bracket the next launch with events
+static void prof_begin(sh_ctx* c, cudaStream_t s) {
+  if (!c->prof_on || c->prof_n >= sh_ctx::PROF_CAP) return;
+  if (!c->ev0[c->prof_n]) cudaEventCreate(&c->ev0[c->prof_n]);
+  cudaEventRecord(c->ev0[c->prof_n], s);
+}
 static void prof_mark(sh_ctx* c, cudaStream_t s, int kind) {
   if (!c->prof_on || c->prof_n >= sh_ctx::PROF_CAP) return;
-  if (!c->ev[c->prof_n + 1]) cudaEventCreate(&c->ev[c->prof_n + 1]);
+  if (!c->ev1[c->prof_n]) cudaEventCreate(&c->ev1[c->prof_n]);
   c->prof_kind[c->prof_n] = kind;
-  cudaEventRecord(c->ev[c->prof_n + 1], s);
+  cudaEventRecord(c->ev1[c->prof_n], s);
   c->prof_n++;
 }
 
@@ -197,9 +203,11 @@ static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min, uint32
 template <int DIM>
 static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
+  prof_begin(c, s);
   k_round<DIM, false><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
+  prof_begin(c, s);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_BOOK);
@@ -209,20 +217,25 @@ static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
 template <int DIM>
 static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
+  prof_begin(c, s);
   k_init<DIM><<<1, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_INIT);
+  prof_begin(c, s);
   k_first_reduce<DIM><<<ws.red_blocks, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_FIRST_REDUCE);
   if (DIM == 3) {
+    prof_begin(c, s);
     k_line_far<<<ws.red_blocks, BLOCK, 0, s>>>(ws);
     CK(cudaGetLastError());
     prof_mark(c, s, KID_LINE_FAR);
   }
+  prof_begin(c, s);
   k_round<DIM, true><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND_FIRST);
+  prof_begin(c, s);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_BOOK);
@@ -232,11 +245,13 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
 template <int DIM>
 static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
   if (DIM == 3) {
+    prof_begin(c, s);
     int rc = filter_launch(c->fws, ws, c->nsm, s);
     if (rc) return rc;
     prof_mark(c, s, KID_FILTER);
     return SH_OK;
   }
+  prof_begin(c, s);
   k_output<DIM><<<c->nsm * 4, BLOCK, 0, s>>>(ws, c->fws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_OUTPUT);
@@ -337,10 +352,6 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     ws.use_cond = 0;
     c->prof_on = (c->launch_mode == 2);
     c->prof_n = 0;
-    if (c->prof_on) {
-      if (!c->ev[0]) cudaEventCreate(&c->ev[0]);
-      cudaEventRecord(c->ev[0], s);
-    }
     rc = launch_pre<DIM>(c, ws, s);
     if (rc) return rc;
     for (;;) {
@@ -451,7 +462,9 @@ void sh_destroy(sh_ctx* c) {
   cudaSetDevice(c->device);
   free_ws(c);
   if (c->st_host) cudaFreeHost(c->st_host);
-  for (auto& e : c->ev)
+  for (auto& e : c->ev0)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev1)
     if (e) cudaEventDestroy(e);
   if (c->build_stream) cudaStreamDestroy(c->build_stream);
   if (c->body_stream) cudaStreamDestroy(c->body_stream);
@@ -535,13 +548,24 @@ int64_t sh_launch_times(sh_ctx* c, int32_t* kind, float* ms, int64_t cap) {
   if (cudaSetDevice(c->device) != cudaSuccess) return 0;
   int64_t n = std::min<int64_t>(c->prof_n, cap);
   for (int64_t i = 0; i < n; i++) {
-    if (cudaEventSynchronize(c->ev[i + 1]) != cudaSuccess) return i;
+    if (cudaEventSynchronize(c->ev1[i]) != cudaSuccess) return i;
     float t = 0.f;
-    cudaEventElapsedTime(&t, c->ev[i], c->ev[i + 1]);
+    cudaEventElapsedTime(&t, c->ev0[i], c->ev1[i]);
     if (kind) kind[i] = c->prof_kind[i];
     if (ms) ms[i] = t;
   }
   return n;
+}
+
+int sh_filter_stats(sh_ctx* c, int64_t* out, int64_t cap) {
+  if (!c || !c->fws.fp || cap <= 0) return 0;
+  FilterParams P;
+  if (cudaMemcpy(&P, c->fws.fp, sizeof(P), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  int64_t v[9] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
+                  (int64_t)P.scanned, (int64_t)P.gjk_iters, 0};
+  int64_t n = std::min<int64_t>(cap, 8);
+  for (int64_t i = 0; i < n; i++) out[i] = v[i];
+  return (int)n;
 }
 
 const char* sh_last_error(void) { return g_last_error.c_str(); }

@@ -87,14 +87,19 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ int classify2(const Seg2& g, double qx, double qy, uint32_t qi,
                                          double* dnext) {
   if (qi == g.fidx) return -1;  // keep[far_seg] = False (:244)
-  // point_in_triangle(ea, eb, fq, q, eps), geometry.py:150-156
-  double d = cross2(g.ax, g.ay, g.bx, g.by, qx, qy);
+  // point_in_triangle(ea, eb, fq, q, eps), geometry.py:150-156, is
+  //   d >= (-eps)|ab|  &  cross2(b, far, q) >= (-eps)|bf|  &  cross2(far, a, q) >= (-eps)|fa|
+  // with d = cross2(a, b, q) > 0 for every live point (by induction: the
+  // first split keeps |d| > eps|pmin pmax| on each side, and a survivor's
+  // next distance is a strictly positive c0 or c1, computed with the very
+  // operation order the next round uses for d), so the first clause is
+  // always true and d is not recomputed.
   // classify_two_edges(a, far, b, q), geometry.py:178-189
   double c0 = cross2(g.ax, g.ay, g.fx, g.fy, qx, qy);  // cross2(a, far, q)
   double c1 = cross2(g.fx, g.fy, g.bx, g.by, qx, qy);  // cross2(far, b, q)
   // cross2(b, far, q) == -c1 and cross2(far, a, q) == -c0 bit-exactly (the
   // symmetric form negates every term exactly, test_geometry.py:35-38)
-  bool inside = (d >= g.nt_ab) & (-c1 >= g.nt_bf) & (-c0 >= g.nt_fa);
+  bool inside = (-c1 >= g.nt_bf) & (-c0 >= g.nt_fa);
   if (inside) return -1;
   bool one_sided = (c0 > 0) != (c1 > 0);
   int state = one_sided ? (c1 > 0 ? 1 : 0) : (c1 > c0 ? 1 : 0);
@@ -108,11 +113,14 @@ __device__ __forceinline__ int classify3(const Seg3& g, double qx, double qy, do
                                          double* dnext) {
   if (g.flat) return -1;          // keep &= ~flat_seg[ids] (:399)
   if (qi == g.fidx) return -1;    // keep[far_seg] = False (:398)
-  double d = plane_dist(g.n, g.a, qx, qy, qz);
+  // base clause d >= (-eps)|n| of point_in_tetrahedron always holds for a
+  // live point (same induction as classify2: side-0 points of the first
+  // split have d >= (-eps)*nlen, the same product; every later distance is
+  // the positive winning D_j, bit-identical to the next round's d)
   double D0 = plane_dist(g.N[0], g.a, qx, qy, qz);
   double D1 = plane_dist(g.N[1], g.b, qx, qy, qz);
   double D2 = plane_dist(g.N[2], g.c, qx, qy, qz);
-  bool inside = (d >= g.nt_base) & (D0 <= g.thr[0]) & (D1 <= g.thr[1]) & (D2 <= g.thr[2]);
+  bool inside = (D0 <= g.thr[0]) & (D1 <= g.thr[1]) & (D2 <= g.thr[2]);
   if (inside) return -1;
   // first argmax of D_j / |N_j| (np.argmax over the stacked quotients)
   double q0 = div_(D0, g.nrm[0]), q1 = div_(D1, g.nrm[1]), q2 = div_(D2, g.nrm[2]);
