@@ -91,6 +91,14 @@ int sh_fetch(sh_ctx* ctx, sh_result* res, void* stream);
 int64_t sh_trace(sh_ctx* ctx, int64_t* live, int64_t* kept, int64_t* nseg, int64_t* flat,
                  int64_t cap);
 
+/* Per-axis bounding box of a point slice (device): out (device, 2*dim
+ * doubles) = min x[,y[,z]], max x[,y[,z]].  Stream-ordered, no host sync.
+ * Sharded hulls all-reduce these boxes (NCCL) and pass the resulting
+ * eps = eps_rel * hypot(spans) as eps_abs, so every shard and the final
+ * merge use the whole input's Tolerance.effective (geometry.py:79-83). */
+int sh_bbox(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride, int64_t n,
+            int dim, double* out, void* stream);
+
 /* Reserve workspace for `dim`-D hulls of up to n points (optional). */
 int sh_reserve(sh_ctx* ctx, int dim, int64_t n);
 

@@ -48,10 +48,11 @@ def lib():
             build()
         L = ctypes.CDLL(_LIB_PATH)
         L.oq_hull2d.restype = ctypes.c_int
-        L.oq_hull2d.argtypes = [_p, _p, _i64, ctypes.c_double, _p, _p, _p, _p, _p, _i64, _p]
+        L.oq_hull2d.argtypes = [_p, _p, _i64, ctypes.c_double, ctypes.c_double, _p, _p, _p, _p, _p,
+                                _i64, _p]
         L.oq_hull3d.restype = ctypes.c_int
-        L.oq_hull3d.argtypes = [_p, _p, _p, _i64, ctypes.c_double, _p, _p, _p, _p, _p, _p, _i64,
-                                _p, _i64, _p]
+        L.oq_hull3d.argtypes = [_p, _p, _p, _i64, ctypes.c_double, ctypes.c_double, _p, _p, _p, _p,
+                                _p, _p, _i64, _p, _i64, _p]
         _lib = L
     return _lib
 
@@ -74,7 +75,7 @@ class OracleResult:
         self.__dict__.update(kw)
 
 
-def hull2d(x, y, eps_rel=1e-12, trace_cap=4096):
+def hull2d(x, y, eps_rel=1e-12, trace_cap=4096, eps_abs=float("nan")):
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
     n = x.size
@@ -82,14 +83,14 @@ def hull2d(x, y, eps_rel=1e-12, trace_cap=4096):
     h, it, tl = (np.zeros(1, np.int64) for _ in range(3))
     fl = np.zeros(1, np.int32)
     tr = np.zeros((trace_cap, 3), np.int64)
-    st = lib().oq_hull2d(_ptr(x), _ptr(y), n, eps_rel, _ptr(out), _ptr(h), _ptr(it), _ptr(fl),
+    st = lib().oq_hull2d(_ptr(x), _ptr(y), n, eps_rel, eps_abs, _ptr(out), _ptr(h), _ptr(it), _ptr(fl),
                          _ptr(tr), trace_cap, _ptr(tl))
     return OracleResult(status=st, idx=out[:h[0]].copy(), iterations=int(it[0]),
                         flags=int(fl[0]), trace=tr[:tl[0]].copy(), filter=0,
                         flat_counts=np.zeros(0, np.int64))
 
 
-def hull3d(x, y, z, eps_rel=1e-12, trace_cap=4096):
+def hull3d(x, y, z, eps_rel=1e-12, trace_cap=4096, eps_abs=float("nan")):
     x, y, z = (np.ascontiguousarray(c, dtype=np.float64) for c in (x, y, z))
     n = x.size
     out = np.zeros(max(n, 1), np.int64)
@@ -98,7 +99,7 @@ def hull3d(x, y, z, eps_rel=1e-12, trace_cap=4096):
     filt = np.zeros(1, np.int32)
     flat = np.zeros(trace_cap, np.int64)
     tr = np.zeros((trace_cap, 3), np.int64)
-    st = lib().oq_hull3d(_ptr(x), _ptr(y), _ptr(z), n, eps_rel, _ptr(out), _ptr(h), _ptr(it),
+    st = lib().oq_hull3d(_ptr(x), _ptr(y), _ptr(z), n, eps_rel, eps_abs, _ptr(out), _ptr(h), _ptr(it),
                          _ptr(fl), _ptr(filt), _ptr(flat), trace_cap, _ptr(tr), trace_cap, _ptr(tl))
     iters = int(it[0])
     return OracleResult(status=st, idx=out[:h[0]].copy(), iterations=iters, flags=int(fl[0]),
@@ -141,11 +142,11 @@ def warnings_3d(res, pruned):
     return w
 
 
-def full_hull3d(x, y, z, eps_rel=1e-12):
+def full_hull3d(x, y, z, eps_rel=1e-12, eps_abs=float("nan")):
     """Loop candidates + Qhull filter: the reference-equivalent 3D result
     (indices in the reference's order) for inputs where the reference's own
     LP filter is infeasible."""
-    r = hull3d(x, y, z, eps_rel)
+    r = hull3d(x, y, z, eps_rel, eps_abs=eps_abs)
     if r.status != STATUS_OK:
         return r, r.idx, []
     idx = r.idx

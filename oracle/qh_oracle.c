@@ -94,7 +94,7 @@ typedef struct { double ax, ay, bx, by; } edge2;
  * reference's discovery order.  trace (optional): 3 int64 per round
  * (live entering, kept after compact, segments).  Returns a status code.
  */
-int oq_hull2d(const double* x0, const double* y0, int64_t n, double eps_rel,
+int oq_hull2d(const double* x0, const double* y0, int64_t n, double eps_rel, double eps_abs,
               int64_t* out_idx, int64_t* out_h, int64_t* out_iters, int32_t* out_flags,
               int64_t* trace, int64_t trace_cap, int64_t* out_trace_len) {
   *out_h = 0;
@@ -103,7 +103,8 @@ int oq_hull2d(const double* x0, const double* y0, int64_t n, double eps_rel,
   if (out_trace_len) *out_trace_len = 0;
   if (n == 0) return OQ_EMPTY;
   const double* cs[2] = {x0, y0};
-  double eps = effective_eps(cs, 2, n, eps_rel);
+  /* eps_abs (not NaN): a sharded run's global eps (paper_1201_2936_b200/sharded.py) */
+  double eps = isnan(eps_abs) ? effective_eps(cs, 2, n, eps_rel) : eps_abs;
   int64_t h = 0;
   int64_t imin = lex_extreme(cs, 2, n, 0);
   int64_t imax = lex_extreme(cs, 2, n, 1);
@@ -306,7 +307,7 @@ static double pdist(const face3* f, double qx, double qy, double qz) {
  * (normal loop exit), 0 for the early returns (result(0)).
  */
 int oq_hull3d(const double* x0, const double* y0, const double* z0, int64_t n, double eps_rel,
-              int64_t* out_idx, int64_t* out_h, int64_t* out_iters, int32_t* out_flags,
+              double eps_abs, int64_t* out_idx, int64_t* out_h, int64_t* out_iters, int32_t* out_flags,
               int32_t* out_filter, int64_t* flat_counts, int64_t flat_cap,
               int64_t* trace, int64_t trace_cap, int64_t* out_trace_len) {
   *out_h = 0;
@@ -316,7 +317,7 @@ int oq_hull3d(const double* x0, const double* y0, const double* z0, int64_t n, d
   if (out_trace_len) *out_trace_len = 0;
   if (n == 0) return OQ_EMPTY;
   const double* cs[3] = {x0, y0, z0};
-  double eps = effective_eps(cs, 3, n, eps_rel);
+  double eps = isnan(eps_abs) ? effective_eps(cs, 3, n, eps_rel) : eps_abs;
   int64_t h = 0;
   int64_t imin = lex_extreme(cs, 3, n, 0);
   int64_t imax = lex_extreme(cs, 3, n, 1);

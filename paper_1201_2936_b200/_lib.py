@@ -19,7 +19,7 @@ SH_FLAG_COLLINEAR = 1
 
 EXPORTED = ("sh_create", "sh_destroy", "sh_hull2d", "sh_hull3d", "sh_hull2d_async",
             "sh_hull3d_async", "sh_fetch", "sh_trace", "sh_reserve", "sh_hypot_host",
-            "sh_set_launch_mode", "sh_launch_times", "sh_filter_stats", "sh_last_error", "sh_version")
+            "sh_set_launch_mode", "sh_launch_times", "sh_filter_stats", "sh_bbox", "sh_last_error", "sh_version")
 
 
 class ShResult(ctypes.Structure):
@@ -78,6 +78,8 @@ def lib():
             L.sh_set_launch_mode.restype = ctypes.c_int
             L.sh_launch_times.argtypes = [P, P, P, I64]
             L.sh_launch_times.restype = I64
+            L.sh_bbox.argtypes = [P, P, P, P, I64, I64, ctypes.c_int, P, P]
+            L.sh_bbox.restype = ctypes.c_int
             L.sh_filter_stats.argtypes = [P, P, I64]
             L.sh_filter_stats.restype = ctypes.c_int
             L.sh_last_error.argtypes = []

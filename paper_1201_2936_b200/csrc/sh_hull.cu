@@ -46,6 +46,7 @@ struct sh_ctx {
   uint64_t cap_n = 0;    // points
   uint32_t segcap = 0;   // segments
   uint32_t mcap = 0;     // 3D filter: candidates
+  unsigned long long* bbox_bits = nullptr;  // sh_bbox scratch
   Workspace ws{};
   FilterWs fws{};
   size_t red_bytes = 0;
@@ -462,6 +463,7 @@ void sh_destroy(sh_ctx* c) {
   cudaSetDevice(c->device);
   free_ws(c);
   if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->bbox_bits) cudaFree(c->bbox_bits);
   for (auto& e : c->ev0)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ev1)
@@ -555,6 +557,22 @@ int64_t sh_launch_times(sh_ctx* c, int32_t* kind, float* ms, int64_t cap) {
     if (ms) ms[i] = t;
   }
   return n;
+}
+
+int sh_bbox(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride, int64_t n,
+            int dim, double* out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if ((dim != 2 && dim != 3) || n <= 0 || !x || !y || (dim == 3 && !z) || !out || stride < 1)
+    return set_err(SH_CONTRACT, "bad bbox arguments");
+  if (n >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "n must be < 2^31");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!c->bbox_bits) CK(cudaMalloc((void**)&c->bbox_bits, 64));
+  k_bbox_init<<<1, 32, 0, s>>>(c->bbox_bits, dim);
+  k_bbox<<<c->nsm * 8, BLOCK, 0, s>>>(x, y, dim == 3 ? z : y, stride, (uint32_t)n, dim, c->bbox_bits);
+  k_bbox_final<<<1, 32, 0, s>>>(c->bbox_bits, out, dim);
+  CK(cudaGetLastError());
+  return SH_OK;
 }
 
 int sh_filter_stats(sh_ctx* c, int64_t* out, int64_t cap) {

@@ -286,6 +286,50 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   }
 }
 
+// ------------------------------------------------------------------ bbox
+// Per-axis min / max of a point slice (sharded hulls all-reduce these to
+// the global Tolerance.effective, geometry.py:79-83).  Ordered-bits atomics
+// into out[0..2*dim): min x[,y[,z]], then max.
+__global__ void __launch_bounds__(BLOCK) k_bbox(const double* px, const double* py, const double* pz,
+                                                int64_t stride, uint32_t n, int dim,
+                                                unsigned long long* out) {
+  unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+  const double* P[3] = {px, py, pz};
+  for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      if (k >= dim) break;
+      const unsigned long long b = ordered_bits(ld_coord(P[k], stride, i));
+      lo[k] = b < lo[k] ? b : lo[k];
+      hi[k] = b > hi[k] ? b : hi[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long a = __shfl_xor_sync(0xFFFFFFFFu, lo[k], o);
+      const unsigned long long b = __shfl_xor_sync(0xFFFFFFFFu, hi[k], o);
+      lo[k] = a < lo[k] ? a : lo[k];
+      hi[k] = b > hi[k] ? b : hi[k];
+    }
+  }
+  if ((threadIdx.x & 31) == 0 && lo[0] != ~0ull) {
+    for (int k = 0; k < dim; k++) {
+      atomicMin(&out[k], lo[k]);
+      atomicMax(&out[dim + k], hi[k]);
+    }
+  }
+}
+
+__global__ void k_bbox_init(unsigned long long* out, int dim) {
+  if (threadIdx.x < 2 * dim) out[threadIdx.x] = threadIdx.x < dim ? ~0ull : 0ull;
+}
+
+__global__ void k_bbox_final(unsigned long long* out, double* res, int dim) {
+  if (threadIdx.x < 2 * dim) res[threadIdx.x] = from_ordered_bits(out[threadIdx.x]);
+}
+
 // ------------------------------------------------------------------ K0b
 struct KeyIdx {
   uint64_t hi;

@@ -56,15 +56,16 @@ def _unit_directions(u):
             np.where(safe, gz / norm, 0.0))
 
 
-def generate(kind, n, seed=0, band=0.01):
-    """SoA tuple of float64 arrays for ``n`` points of ``kind``."""
+def generate(kind, n, seed=0, band=0.01, start=0):
+    """SoA tuple of float64 arrays for ``n`` points of ``kind``: points
+    start..start+n-1 of the seeded cloud (a shard of a larger cloud)."""
     if kind not in _DRAWS:
         raise ValueError(f"unknown distribution kind {kind!r}")
     dim = 2 if kind in KINDS_2D else 3
     if n == 0:
         return tuple(np.empty(0, np.float64) for _ in range(dim))
     cols = _DRAWS[kind]
-    u = uniform_stream(seed, n * cols).reshape(n, cols)
+    u = uniform_stream(seed, n * cols, start=1 + start * cols).reshape(n, cols)
     if kind in ("unit-square", "unit-cube"):
         return tuple(np.ascontiguousarray(u[:, j]) for j in range(cols))
     if kind == "uniform-disk":
