@@ -32,9 +32,10 @@ struct BookShared {
   Sum3 agg, prefix;
   int stop[4];
   // children spanning many next-round tiles: their tile_seg entries are
-  // filled by the whole block
+  // filled by the whole block (flattened over an inclusive prefix of
+  // their tile counts)
   uint32_t nfill;
-  uint32_t fill_seg[TILE3], fill_t0[TILE3], fill_n[TILE3];
+  uint32_t fill_seg[TILE3], fill_t0[TILE3], fill_n[TILE3], fill_pre[TILE3];
 };
 
 template <int DIM>
@@ -264,9 +265,37 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
     }
 
     __syncthreads();
-    for (uint32_t q = 0; q < sb.nfill; q++) {
-      const uint32_t c = sb.fill_seg[q], t0 = sb.fill_t0[q], nt = sb.fill_n[q];
-      for (uint32_t t = tid; t < nt; t += BLOCK) tile_seg[t0 + t] = c;
+    {
+      const uint32_t nf = sb.nfill;
+      if (nf) {
+        // inclusive prefix of the tile counts (one warp), then one thread per tile
+        if (warp == 0) {
+          uint32_t carry = 0;
+          for (uint32_t q0 = 0; q0 < nf; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            uint32_t v = q < nf ? sb.fill_n[q] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+              if (lane >= o) v += y;
+            }
+            if (q < nf) sb.fill_pre[q] = carry + v;
+            carry += __shfl_sync(0xFFFFFFFFu, v, 31);
+          }
+        }
+        __syncthreads();
+        const uint32_t total = sb.fill_pre[nf - 1];
+        for (uint32_t k = tid; k < total; k += BLOCK) {
+          uint32_t lo = 0, hi = nf - 1;  // first q with fill_pre[q] > k
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sb.fill_pre[mid] > k) hi = mid;
+            else lo = mid + 1;
+          }
+          const uint32_t before = lo ? sb.fill_pre[lo - 1] : 0u;
+          tile_seg[sb.fill_t0[lo] + (k - before)] = sb.fill_seg[lo];
+        }
+      }
     }
 
     // ---- finalise the launch: next round's parameters + loop condition

@@ -52,9 +52,12 @@ struct RoundShared {
   uint32_t wstart[2][WMAX + 2];      // window: dense start of every segment (+ next)
   unsigned long long wphys[2][WMAX + 1];  // window: physical offset of every segment
   uint32_t wlo[2], wn[2], wslow[2];
+  uint32_t wslot[2][RTILE / 32];     // window segment of each 32-point slot's first point
+  __align__(16) unsigned long long seg0[2][(sizeof(Seg3) + 15) / 16 * 2];  // first segment's table
   uint32_t kcnt[WMAX * DIM];         // per (window segment, state) of the current tile
   uint32_t kbase[WMAX * DIM];
-  unsigned long long khi[WMAX * DIM];
+  uint32_t khh[WMAX * DIM];          // farthest key, upper / lower 32 bits
+  uint32_t khl[WMAX * DIM];
   uint32_t kidx[WMAX * DIM];
   uint32_t pend_seg[2];              // segment carried into the next tile (by tile parity)
   uint32_t pend_complete[2];         // its aggregate covers it from its first point
@@ -216,6 +219,16 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     if (!slow) {
       for (uint32_t w = lane; w <= nw; w += 32) S.wstart[b][w] = segstart[lo + w];
       for (uint32_t w = lane; w < nw; w += 32) S.wphys[b][w] = seg_phys[lo + w];
+      __syncwarp();
+      // one binary search per 32-point slot (all slots at once, one per lane)
+      const uint32_t q = t * RTILE + lane * 32;
+      S.wslot[b][lane] = q < n_live ? win_search(S.wstart[b], nw, q) : 0u;
+    }
+    {
+      using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ws.seg[cur]) +
+                                      (size_t)lo * (sizeof(SegT) / 8);
+      for (uint32_t k = lane; k < sizeof(SegT) / 8; k += 32) S.seg0[b][k] = src[k];
     }
     if (lane == 0) {
       S.wlo[b] = lo;
@@ -280,6 +293,17 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     for (int j = 0; j < RITEMS; j++) {
       const uint32_t i = j * RB + tid;
       const uint32_t q = base + i;
+      uint32_t wfast = 0;
+      if (!FIRST && !contig && !slow) {
+        // segment of q: the slot's first segment + the starts inside the slot
+        const uint32_t wb = S.wslot[b][i >> 5];
+        const uint32_t slot0 = base + (i & ~31u);
+        const uint32_t k = wb + 1 + lane;
+        const uint32_t off = (k <= nw) ? S.wstart[b][k] - slot0 : 32u;
+        const uint32_t m = __reduce_or_sync(0xFFFFFFFFu, off < 32u ? (1u << off) : 0u);
+        const uint32_t le = (lane == 31) ? 0xFFFFFFFFu : ((2u << lane) - 1u);
+        wfast = wb + __popc(m & le);
+      }
       if (i >= cnt) continue;
       if (FIRST) {
         const int64_t o = (int64_t)q * pstride;
@@ -295,7 +319,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         uint32_t w;
         uint64_t phys;
         if (!slow) {
-          w = win_search(S.wstart[b], nw, q);
+          w = wfast;
           phys = S.wphys[b][w] + (q - S.wstart[b][w]);
         } else {
           w = win_search(segstart + lo, nw, q);
@@ -315,7 +339,8 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   if (tid < K * WMAX) {
     for (uint32_t e = tid; e < (uint32_t)(K * WMAX); e += RB) {
       S.kcnt[e] = 0;
-      S.khi[e] = 0ull;
+      S.khh[e] = 0u;
+      S.khl[e] = 0u;
       S.kidx[e] = 0xFFFFFFFFu;
     }
   }
@@ -399,7 +424,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     const SegT* segtab = reinterpret_cast<const SegT*>(ws.seg[cur]);
     if (FIRST || (uniform && !slow)) {
       SegT g0;
-      if (!FIRST) g0 = segtab[lo];  // one table load per thread per tile
+      if (!FIRST) g0 = *reinterpret_cast<const SegT*>(S.seg0[b]);  // staged with the window
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) classify_item(j, true, [&](uint32_t) -> const SegT& { return g0; });
     } else {
@@ -539,6 +564,8 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       if (tid == 0 && !(has_next && S.wstart[b][nw] > tile_end)) S.pend_seg[pout] = NOKEY;
     } else if (!slow) {
       // ---- per (segment, state): tile-local ranks, counts, farthest keys
+      // (upper 32 bits of the key by shared atomicMax now, lower 32 bits
+      // among the upper-bit winners after the barrier: native 32-bit atomics)
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
         const uint32_t i = j * RB + tid;
@@ -546,6 +573,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         const uint32_t w = valid ? (uint32_t)sw[i] : 0u;
         const uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, valid ? w : 0xFFFFu);
         const uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, valid ? w : 0u);
+        const uint32_t hu = (uint32_t)(khi_[j] >> 32);
         if (wmin == wmax) {
           // one segment in this 32-point slot: ballots + REDUX per state
 #pragma unroll
@@ -554,15 +582,12 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
             const bool mine = key[j] == kk;
             const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
             if (!m) continue;
-            const uint32_t hu = mine ? (uint32_t)(khi_[j] >> 32) : 0u;
-            const uint32_t mu = __reduce_max_sync(0xFFFFFFFFu, hu);
-            const uint32_t hl = (mine && hu == mu) ? (uint32_t)khi_[j] : 0u;
-            const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, hl);
+            const uint32_t mu = __reduce_max_sync(0xFFFFFFFFu, mine ? hu : 0u);
             const int leader = __ffs(m) - 1;
             uint32_t off = 0;
             if (lane == leader) {
               off = atomicAdd(&S.kcnt[kk], (uint32_t)__popc(m));
-              atomicMax(&S.khi[kk], ((unsigned long long)mu << 32) | ml);
+              atomicMax(&S.khh[kk], mu);
             }
             off = __shfl_sync(0xFFFFFFFFu, off, leader);
             if (mine) rank[j] = off + __popc(m & lanemask_lt());
@@ -575,16 +600,16 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
           off = __shfl_sync(0xFFFFFFFFu, off, leader);
           if (key[j] != NOKEY) {
             rank[j] = off + __popc(grp & lanemask_lt());
-            atomicMax(&S.khi[key[j]], khi_[j]);
+            atomicMax(&S.khh[key[j]], hu);
           }
         }
       }
       __syncthreads();
-      // ---- lowest index among the farthest; one global claim per child
+      // ---- lower key bits among the upper-bit winners; one global claim per child
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
-        if (key[j] != NOKEY && khi_[j] == S.khi[key[j]])
-          atomicMin(&S.kidx[key[j]], FIRST ? tile_begin + j * RB + tid : si[j * RB + tid]);
+        if (key[j] != NOKEY && (uint32_t)(khi_[j] >> 32) == S.khh[key[j]])
+          atomicMax(&S.khl[key[j]], (uint32_t)khi_[j]);
       }
       const uint32_t ne = nw * K;
       for (uint32_t e = tid; e < ne; e += RB) {
@@ -592,23 +617,29 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         if (c) S.kbase[e] = atomicAdd(&cursor[(size_t)(lo + e / K) * K + e % K], c);
       }
       __syncthreads();
-      // ---- write the survivors
+      // ---- lowest index among the farthest; write the survivors
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
         if (key[j] == NOKEY) continue;
         const uint32_t i = j * RB + tid;
-        const uint32_t s = key[j] % K;
-        const size_t dst = (size_t)s * rcap + S.kbase[key[j]] + rank[j];
+        const uint32_t kk = key[j];
+        const uint32_t qi = FIRST ? (tile_begin + i) : si[i];
+        if ((uint32_t)(khi_[j] >> 32) == S.khh[kk] && (uint32_t)khi_[j] == S.khl[kk]) atomicMin(&S.kidx[kk], qi);
+        const uint32_t s = kk % K;
+        const size_t dst = (size_t)s * rcap + S.kbase[kk] + rank[j];
         outx[dst] = sx[i];
         outy[dst] = sx[RTILE + i];
         if (DIM == 3) outz[dst] = sx[2 * RTILE + i];
-        outi[dst] = FIRST ? (tile_begin + i) : si[i];
+        outi[dst] = qi;
       }
+      __syncthreads();
       // ---- close, carry or merge every child of the tile
       for (uint32_t e = tid; e < ne; e += RB) {
-        close_child(e / K, e % K, S.kcnt[e] ? S.khi[e] : 0ull, S.kidx[e]);
+        close_child(e / K, e % K,
+                    S.kcnt[e] ? (((unsigned long long)S.khh[e] << 32) | S.khl[e]) : 0ull, S.kidx[e]);
         S.kcnt[e] = 0;
-        S.khi[e] = 0ull;
+        S.khh[e] = 0u;
+        S.khl[e] = 0u;
         S.kidx[e] = 0xFFFFFFFFu;
       }
       if (tid == 0 && !(has_next && S.wstart[b][nw] > tile_end)) S.pend_seg[pout] = NOKEY;
