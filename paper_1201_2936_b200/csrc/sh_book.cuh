@@ -31,11 +31,6 @@ struct BookShared {
   uint32_t wsum[ITEMS3 * WARPS * 3];
   Sum3 agg, prefix;
   int stop[4];
-  // children spanning many next-round tiles: their tile_seg entries are
-  // filled by the whole block (flattened over an inclusive prefix of
-  // their tile counts)
-  uint32_t nfill;
-  uint32_t fill_seg[TILE3], fill_t0[TILE3], fill_n[TILE3], fill_pre[TILE3];
 };
 
 template <int DIM>
@@ -45,11 +40,20 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
   __shared__ BookShared sb;
   __shared__ RoundParams s_rp;
   __shared__ uint32_t s_seq;
+  __shared__ Sum3 s_carry;
+  // few children (flag written by the round kernel): block 0 does everything
+  // in tile order with a running prefix -- no look-back, no arrival protocol
+  const bool small = st->book_small != 0;
+  if (small && blockIdx.x != 0) return;
   if (threadIdx.x == 0) {
     s_rp = st->rp;
     s_seq = st->seq;
-    __threadfence();
-    atomicAdd(&st->arrive_book, 1u);  // the finaliser waits for every block's read
+    s_carry = s3_identity();
+    if (!small) {
+      __threadfence();
+      atomicAdd(&st->arrive_book, 1u);  // the finaliser waits for every block's read
+    }
+    sb.tile = 0xFFFFFFFFu;
   }
   __syncthreads();
   const RoundParams bp = s_rp;
@@ -74,17 +78,15 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
   uint32_t* segstart = ws.segstart[out_b];
   uint64_t* seg_phys = ws.seg_phys[out_b];
   uint32_t* cur_out = ws.cursor[out_b];
-  uint32_t* tile_seg = ws.tile_seg[out_b];
 
   while (true) {
-    if (tid == 0) sb.tile = atomicAdd(&st->ctr_book, 1u);
+    if (tid == 0) sb.tile = small ? sb.tile + 1u : atomicAdd(&st->ctr_book, 1u);
     __syncthreads();
     const uint32_t tile = sb.tile;
     if (tile >= num_tiles) break;
     const uint32_t base = tile * TILE3;
     const bool last_tile = tile == num_tiles - 1;
 
-    if (tid == 0) sb.nfill = 0;
     RunVal v[ITEMS3];
     uint32_t cval[ITEMS3][3];
     // 3D child face (needed before the scan for the flat test)
@@ -171,7 +173,9 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       }
     }
     __syncthreads();
-    if (tile > 0) {
+    if (small) {
+      if (tid < 3) sb.prefix.v[tid] = s_carry.v[tid];
+    } else if (tile > 0) {
       if (tid == 0) lb_publish<3>(ws.lb_book, tile, tag16, LB_AGG, sb.agg.v);
       lb_lookback<3>(ws.lb_book, tile, tag16, sb.prefix.v, sb.stop);
     } else if (tid < 3) {
@@ -180,7 +184,8 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
     __syncthreads();
     if (tid == 0) {
       Sum3 inc = s3_combine(sb.prefix, sb.agg);
-      lb_publish<3>(ws.lb_book, tile, tag16, LB_INC, inc.v);
+      if (small) s_carry = inc;
+      else lb_publish<3>(ws.lb_book, tile, tag16, LB_INC, inc.v);
     }
 
     // ---- build child tables, emit vertices
@@ -200,17 +205,6 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       seg_phys[c] = (uint64_t)s * rcap + __ldg(&par_start[p]);  // where K2 wrote child (p, s)
 #pragma unroll
       for (int q = 0; q < K; q++) cur_out[(size_t)c * K + q] = start;
-      {  // first segment of every next-round tile that starts inside [start, start+cnt)
-        uint32_t t0 = (start + RTILE - 1) / RTILE, t1 = (start + v[j].cnt - 1) / RTILE;
-        if (t1 >= t0 + 8) {
-          uint32_t q = atomicAdd(&sb.nfill, 1u);
-          sb.fill_seg[q] = c;
-          sb.fill_t0[q] = t0;
-          sb.fill_n[q] = t1 - t0 + 1;
-        } else {
-          for (uint32_t t = t0; t <= t1; t++) tile_seg[t] = c;
-        }
-      }
       double F[3];
       F[0] = ld_coord(st->px, stride, far);
       F[1] = ld_coord(st->py, stride, far);
@@ -265,38 +259,6 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
     }
 
     __syncthreads();
-    {
-      const uint32_t nf = sb.nfill;
-      if (nf) {
-        // inclusive prefix of the tile counts (one warp), then one thread per tile
-        if (warp == 0) {
-          uint32_t carry = 0;
-          for (uint32_t q0 = 0; q0 < nf; q0 += 32) {
-            const uint32_t q = q0 + lane;
-            uint32_t v = q < nf ? sb.fill_n[q] : 0u;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
-              if (lane >= o) v += y;
-            }
-            if (q < nf) sb.fill_pre[q] = carry + v;
-            carry += __shfl_sync(0xFFFFFFFFu, v, 31);
-          }
-        }
-        __syncthreads();
-        const uint32_t total = sb.fill_pre[nf - 1];
-        for (uint32_t k = tid; k < total; k += BLOCK) {
-          uint32_t lo = 0, hi = nf - 1;  // first q with fill_pre[q] > k
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (sb.fill_pre[mid] > k) hi = mid;
-            else lo = mid + 1;
-          }
-          const uint32_t before = lo ? sb.fill_pre[lo - 1] : 0u;
-          tile_seg[sb.fill_t0[lo] + (k - before)] = sb.fill_seg[lo];
-        }
-      }
-    }
 
     // ---- finalise the launch: next round's parameters + loop condition
     if (last_tile && tid == 0) {
@@ -305,8 +267,9 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
       uint32_t status = st->status;
       uint32_t round_next = bp.round + 1;  // the round the children belong to
       // every block has read this round's parameters before they change
-      while (*(volatile uint32_t*)&st->arrive_book < gridDim.x) {
-      }
+      if (!small)
+        while (*(volatile uint32_t*)&st->arrive_book < gridDim.x) {
+        }
       if (bp.root && DIM == 3) {
         // quickhull.py:349-351 -- every point within eps of the first plane
         double dmax = __longlong_as_double((long long)st->dmax_bits);

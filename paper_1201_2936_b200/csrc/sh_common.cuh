@@ -41,6 +41,7 @@ constexpr int RB = 256;              // threads per round-kernel block
 constexpr int RITEMS = 4;            // points per thread per round tile
 constexpr int RTILE = RB * RITEMS;   // 1024 points per round tile
 constexpr int WMAX = 256;            // tile-window segments kept in shared memory
+constexpr uint32_t BOOK_SMALL = 1024; // children handled by a single K3 block
 
 // status codes (C ABI, include/seghull_b200.h)
 constexpr uint32_t ST_OK = 0;
@@ -159,7 +160,7 @@ struct DevState {
   uint32_t ctr_book;      // dynamic tile counter of K3 (reset by K2)
   uint32_t arrive_book;   // K3 blocks that have read rp (reset by K3's finalizer)
   uint32_t ctr_red;       // last-block counter for reductions
-  uint32_t pad0;
+  uint32_t book_small;    // K3 runs in one block (few children); set by K2
   // ---- traces (per round r, index r-1) ----
   uint32_t tr_live[MAX_TRACE];
   uint32_t tr_kept[MAX_TRACE];
@@ -180,7 +181,6 @@ struct Workspace {
   void* seg[2];
   uint32_t* segstart[2];   // dense logical start (+ sentinel = n_live)
   uint64_t* seg_phys[2];   // physical element offset of the first record
-  uint32_t* tile_seg[2];   // first segment of every round tile
   // per child (e = parent*K + state) of the round reading buffer b:
   uint32_t* cursor[2];     // write cursor, initialised to the parent's start
   Key128* slot_key;        // farthest key, zero between uses

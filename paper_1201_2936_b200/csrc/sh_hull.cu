@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -75,6 +76,17 @@ static void prof_begin(sh_ctx* c, cudaStream_t s) {
   cudaEventRecord(c->ev0[c->prof_n], s);
 }
 static void prof_mark(sh_ctx* c, cudaStream_t s, int kind) {
+  static const bool dbg = getenv("SH_DEBUG") != nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (dbg) cudaStreamIsCapturing(s, &cap);
+  if (dbg && c->launch_mode != 0 && cap == cudaStreamCaptureStatusNone) {  // debugging aid
+    cudaError_t e = cudaStreamSynchronize(s);
+    DevState h;
+    cudaMemcpy(&h, c->ws.st, offsetof(DevState, tr_live), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[sh] kernel %d done (%s): rp active=%u root=%u n_live=%u nseg=%u cur=%u round=%u status=%u\n",
+            kind, cudaGetErrorString(e), h.rp.active, h.rp.root, h.rp.n_live, h.rp.nseg, h.rp.cur, h.rp.round,
+            h.status);
+  }
   if (!c->prof_on || c->prof_n >= sh_ctx::PROF_CAP) return;
   if (!c->ev1[c->prof_n]) cudaEventCreate(&c->ev1[c->prof_n]);
   c->prof_kind[c->prof_n] = kind;
@@ -112,7 +124,6 @@ static void free_ws(sh_ctx* c) {
     cudaFree(w.segstart[b]);
     cudaFree(w.seg_phys[b]);
     cudaFree(w.cursor[b]);
-    cudaFree(w.tile_seg[b]);
   }
   cudaFree(w.slot_key);
   cudaFree(w.lb_book);
@@ -151,7 +162,6 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
     ok &= dalloc(&w.segstart[b], (size_t)segcap + 4) == cudaSuccess;
     ok &= dalloc(&w.seg_phys[b], (size_t)segcap + 4) == cudaSuccess;
     ok &= dalloc(&w.cursor[b], (size_t)K * segcap + 4) == cudaSuccess;
-    ok &= dalloc(&w.tile_seg[b], max_tiles + 4) == cudaSuccess;
   }
   ok &= dalloc(&w.slot_key, (size_t)K * segcap + 4) == cudaSuccess;
   ok &= dalloc(&w.lb_book, book_tiles * 4) == cudaSuccess;

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
     st->first_active = 0;
     st->ctr_book = 0;
     st->arrive_book = 0;
+    st->book_small = 1;
     st->ctr_red = 0;
     st->dmax_bits = 0;
     st->rp.active = 0;

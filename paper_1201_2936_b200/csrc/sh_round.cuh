@@ -51,7 +51,7 @@ template <int DIM>
 struct RoundShared {
   uint32_t wstart[2][WMAX + 2];      // window: dense start of every segment (+ next)
   unsigned long long wphys[2][WMAX + 1];  // window: physical offset of every segment
-  uint32_t wlo[2], wn[2], wslow[2];
+  uint32_t wlo[2], wn[2], wslow[2], wnext[2];
   uint32_t wslot[2][RTILE / 32];     // window segment of each 32-point slot's first point
   __align__(16) unsigned long long seg0[2][(sizeof(Seg3) + 15) / 16 * 2];  // first segment's table
   uint32_t kcnt[WMAX * DIM];         // per (window segment, state) of the current tile
@@ -156,7 +156,11 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
 
   const RoundParams rp = st->rp;
   if (!rp.active || (rp.root != 0) != FIRST) return;
-  if (blockIdx.x == 0 && tid == 0) st->ctr_book = 0;  // K3's tile counter
+  if (blockIdx.x == 0 && tid == 0) {
+    st->ctr_book = 0;  // K3's tile counter
+    st->arrive_book = 0;
+    st->book_small = (uint32_t)K * rp.nseg <= BOOK_SMALL ? 1u : 0u;
+  }
   const uint32_t n_live = rp.n_live, nseg = rp.nseg, cur = rp.cur;
   const uint32_t num_tiles = (n_live + RTILE - 1) / RTILE;
   const uint32_t t0 = (uint32_t)(((uint64_t)num_tiles * blockIdx.x) / gridDim.x);
@@ -173,7 +177,6 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   uint32_t* outi = ws.ri[cur ^ 1u];
   const uint32_t* segstart = ws.segstart[cur];
   const uint64_t* seg_phys = ws.seg_phys[cur];
-  const uint32_t* tile_seg = ws.tile_seg[cur];
   uint32_t* cursor = ws.cursor[cur];
 
   // first-split constants
@@ -200,6 +203,27 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   auto stage_ptr = [&](uint32_t b) { return dsm + (size_t)b * RoundSmem<DIM>::stage_bytes(); };
 
   // ---- window of tile t into buffer b (warp 0)
+  // segment containing logical position q (warp-cooperative 32-ary search)
+  auto find_segment = [&](uint32_t q) -> uint32_t {
+    uint32_t lo = 0, hi = nseg - 1;
+    while (hi - lo > 31u) {
+      const uint32_t step = (hi - lo + 32u) / 32u;  // ceil(range size / 32)
+      const uint32_t idx = lo + lane * step;  // probes beyond hi do not vote
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, idx <= hi && segstart[idx] <= q);
+      const uint32_t L = 31u - __clz(m);
+      const uint32_t nlo = lo + L * step;
+      hi = min(hi, nlo + step - 1u);
+      lo = nlo;
+    }
+    const uint32_t idx = lo + lane;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, idx <= hi && segstart[idx] <= q);
+    return lo + (31u - __clz(m));
+  };
+
+  // ---- window of tile t into buffer b (warp 0): every segment overlapping
+  // the tile, found by scanning segstart forward from the tile's first
+  // segment (carried from the previous tile's window; a 32-ary search for a
+  // block's first tile)
   auto load_window = [&](uint32_t t, uint32_t b) {
     if (FIRST) {
       if (lane == 0) {
@@ -212,16 +236,29 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       }
       return;
     }
-    const uint32_t lo = tile_seg[t];
-    const uint32_t hi = (t + 1 < num_tiles) ? tile_seg[t + 1] : nseg - 1;
-    const uint32_t nw = hi - lo + 1;
+    const uint32_t base = t * RTILE, end = min(base + (uint32_t)RTILE, n_live);
+    const uint32_t lo = (t == t0) ? find_segment(base) : S.wnext[b ^ 1u];
+    uint32_t nw = 0, nxt = lo;
+    for (uint32_t w0 = 0;; w0 += 32) {
+      const uint32_t idx = lo + w0 + lane;
+      const uint32_t st_ = idx <= nseg ? segstart[idx] : 0xFFFFFFFFu;  // segstart[nseg] = n_live
+      if (w0 + lane <= (uint32_t)WMAX) S.wstart[b][w0 + lane] = st_;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, st_ < end);
+      if (m != 0xFFFFFFFFu) {
+        const uint32_t c = __popc(m);  // segments of this batch that start inside the tile
+        nw = w0 + c;
+        // first position of the next tile: in segment lo+nw-1, or lo+nw when it starts there
+        const uint32_t nstart = __shfl_sync(0xFFFFFFFFu, st_, c & 31u);
+        nxt = lo + nw - 1 + ((c < 32u && nstart == end) ? 1u : 0u);
+        break;
+      }
+    }
     const bool slow = nw > (uint32_t)WMAX;
     if (!slow) {
-      for (uint32_t w = lane; w <= nw; w += 32) S.wstart[b][w] = segstart[lo + w];
       for (uint32_t w = lane; w < nw; w += 32) S.wphys[b][w] = seg_phys[lo + w];
       __syncwarp();
       // one binary search per 32-point slot (all slots at once, one per lane)
-      const uint32_t q = t * RTILE + lane * 32;
+      const uint32_t q = base + lane * 32;
       S.wslot[b][lane] = q < n_live ? win_search(S.wstart[b], nw, q) : 0u;
     }
     {
@@ -234,6 +271,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       S.wlo[b] = lo;
       S.wn[b] = nw;
       S.wslow[b] = slow ? 1u : 0u;
+      S.wnext[b] = nxt;
     }
   };
 
