@@ -54,6 +54,7 @@ struct FilterParams {
   uint32_t lnodes[F_LEVELS];   // nodes per tree level
   uint32_t loff[F_LEVELS];     // first node of each level in nbox
   double lo[3], inv_h[3], ctr[3];
+  double gsum[3];              // sum of the candidates (deterministic order)
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
   uint32_t ambiguous, gjk_capped, pad0, pad1;
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
@@ -374,10 +375,32 @@ __global__ void __launch_bounds__(1024) k_f_boxes01(FilterWs f) {
   }
 }
 
-// levels 2.. (at most a few hundred nodes): one block, one warp per node
+// levels 2.. (at most a few hundred nodes): one block, one warp per node;
+// the same block also sums the candidates in a fixed order (centroid)
 __global__ void __launch_bounds__(1024) k_f_boxes_hi(FilterWs f) {
   const FilterParams* P = f.fp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    __shared__ double s_sum[32][3];
+    double a[3] = {0.0, 0.0, 0.0};
+    for (uint32_t p = threadIdx.x; p < P->m; p += 1024) {
+      a[0] += f.cx[p];
+      a[1] += f.cy[p];
+      a[2] += f.cz[p];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      for (int o = 16; o; o >>= 1) a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], o);
+    if (lane == 0)
+      for (int k = 0; k < 3; k++) s_sum[warp][k] = a[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t[3] = {0.0, 0.0, 0.0};
+      for (int w = 0; w < 32; w++)
+        for (int k = 0; k < 3; k++) t[k] += s_sum[w][k];
+      for (int k = 0; k < 3; k++) f.fp->gsum[k] = t[k];
+    }
+  }
   for (int l = 2; l < (int)P->nlev; l++) {
     const uint32_t nl = P->lnodes[l], nc = P->lnodes[l - 1];
     for (uint32_t node = warp; node < nl; node += 32) {
@@ -690,46 +713,37 @@ __device__ __forceinline__ double tet_depth(const V3* W) {
   return dmin;
 }
 
-// 1 keep, 0 prune; *amb set when kept only because v is within eps of the
-// boundary of the other candidates' hull (or the iteration cap was hit).
-__device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t i, V3 v, V3 ctr, double eps,
-                        int* amb, int* capped, FStack& stk, FStat& fs) {
-  V3 w0 = vsub(v, ctr);
-  double wl = sqrt_(vdot(w0, w0));
-  if (!(wl > 0.0)) {
-    w0 = v3(1.0, 0.0, 0.0);
-    wl = 1.0;
-  }
-  // (1) certificate along v - centre
-  const double thr0 = mul(eps, wl);
-  Sup s = support_query(f, P, w0, v, i, thr0, true, stk, fs);
-  if (!(s.val > thr0)) {
-    fs.certified++;
-    return 1;
-  }
-  // (2) GJK on U = {c - v : c != v}
+// GJK distance test of the origin against conv(U), U given by a support
+// oracle sup(dir) -> (value, id, u) maximising dir.u.  Outcomes:
+enum { GJK_OUTSIDE = 0, GJK_INSIDE = 1, GJK_AMBIGUOUS = 2, GJK_CAPPED = 3 };
+struct SupU {
+  double val;
+  uint32_t id;  // 0xFFFFFFFF: empty set
+  V3 u;
+};
+
+template <class SupFn>
+__device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters) {
   V3 W[4];
   uint32_t id[4];
   int n = 1;
-  W[0] = vsub(v3(f.sx[s.pos], f.sy[s.pos], f.sz[s.pos]), v);
-  id[0] = s.id;
+  W[0] = first.u;
+  id[0] = first.id;
   V3 x = W[0];
 #pragma unroll 1
   for (int it = 0; it < 64; it++) {
-    double xx = vdot(x, x);
-    if (xx <= 0.0) {
-      *amb = 1;
-      return 1;
-    }
-    V3 dir = vneg(x);
-    fs.iters++;
-    Sup q = support_query(f, P, dir, v, i, 0.0, false, stk, fs);
-    if (q.pos == 0xFFFFFFFFu) return 1;
+    const double xx = vdot(x, x);
+    if (xx <= 0.0) return GJK_AMBIGUOUS;
+    const V3 dir = vneg(x);
+    (*iters)++;
+    const SupU q = sup(dir);
+    *sep = dir;
+    if (q.id == 0xFFFFFFFFu) return GJK_OUTSIDE;
     // q.val = max_u (-x).u ; gap = x.x - min_u x.u = xx + q.val
-    if (add(xx, q.val) <= 1e-13 * xx) return 1;  // origin outside: v is extreme
+    if (add(xx, q.val) <= 1e-13 * xx) return GJK_OUTSIDE;
     for (int k = 0; k < n; k++)
-      if (id[k] == q.id) return 1;               // no progress: outside
-    W[n] = vsub(v3(f.sx[q.pos], f.sy[q.pos], f.sz[q.pos]), v);
+      if (id[k] == q.id) return GJK_OUTSIDE;  // no progress
+    W[n] = q.u;
     id[n] = q.id;
     n++;
     if (n == 2) {
@@ -738,26 +752,146 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t i, V3
       x = closest_tri(W, id, n);
     } else {
       bool degen = false;
-      if (closest_tet(W, id, n, x, degen)) {
-        if (tet_depth(W) > eps) return 0;        // strictly inside: prune
-        *amb = 1;
-        return 1;
-      }
-      if (degen) {
-        *amb = 1;
-        return 1;
+      if (closest_tet(W, id, n, x, degen)) return tet_depth(W) > eps ? GJK_INSIDE : GJK_AMBIGUOUS;
+      if (degen) return GJK_AMBIGUOUS;
+    }
+    if (sqrt_(vdot(x, x)) <= eps) return GJK_AMBIGUOUS;  // within eps of the boundary
+  }
+  return GJK_CAPPED;
+}
+
+constexpr int F_LOCAL = 3;  // local set: 3 * 32 sorted neighbours of the candidate
+
+// 1 keep, 0 prune; *amb set when kept only because v is within eps of the
+// boundary of the other candidates' hull (or the iteration cap was hit).
+__device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, uint32_t i, V3 v, V3 ctr,
+                        V3 gsum, double eps, int* amb, int* capped, FStack& stk, FStat& fs) {
+  const int lane = threadIdx.x & 31;
+  V3 w0 = vsub(v, ctr);
+  double wl = sqrt_(vdot(w0, w0));
+  if (!(wl > 0.0)) {
+    w0 = v3(1.0, 0.0, 0.0);
+    wl = 1.0;
+  }
+  // (0) certificate along v - centre (one existence query)
+  const double thr0 = mul(eps, wl);
+  const Sup s0 = support_query(f, P, w0, v, i, thr0, true, stk, fs);
+  if (!(s0.val > thr0)) {
+    fs.certified++;
+    return 1;
+  }
+  int iters = 0;
+  // (1) local GJK: the candidate's Morton neighbours plus the centroid of
+  // all other candidates (a convex combination of them, so any simplex it
+  // spans with candidates lies in their hull)
+  {
+    const uint32_t lo = ps > 16u * F_LOCAL ? ps - 16u * F_LOCAL : 0u;
+    V3 lu[F_LOCAL];
+    uint32_t lid[F_LOCAL];
+#pragma unroll
+    for (int k = 0; k < F_LOCAL; k++) {
+      const uint32_t p = lo + k * 32 + lane;
+      lid[k] = 0xFFFFFFFFu;
+      lu[k] = v3(0.0, 0.0, 0.0);
+      if (p < P.m && p != ps) {
+        lid[k] = __ldg(&f.sid[p]);
+        lu[k] = vsub(v3(__ldg(&f.sx[p]), __ldg(&f.sy[p]), __ldg(&f.sz[p])), v);
       }
     }
-    if (sqrt_(vdot(x, x)) <= eps) {
-      *amb = 1;                                  // within eps of the boundary
-      return 1;
+    const double inv = 1.0 / (double)(P.m - 1);
+    const V3 g = vsub(v3(mul(sub(gsum.x, v.x), inv), mul(sub(gsum.y, v.y), inv), mul(sub(gsum.z, v.z), inv)), v);
+    auto local_sup = [&](V3 d) -> SupU {
+      double bv = -INFINITY;
+      uint32_t bid = 0xFFFFFFFFu;
+      int bk = -1;
+#pragma unroll
+      for (int k = 0; k < F_LOCAL; k++) {
+        const double val = vdot(d, lu[k]);
+        if (lid[k] != 0xFFFFFFFFu && (val > bv || (val == bv && lid[k] < bid))) {
+          bv = val;
+          bid = lid[k];
+          bk = k;
+        }
+      }
+      if (lane == 0) {  // the centroid, id 0xFFFFFFFE
+        const double val = vdot(d, g);
+        if (val > bv) {
+          bv = val;
+          bid = 0xFFFFFFFEu;
+          bk = F_LOCAL;
+        }
+      }
+      int bl = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bid, o);
+        const int ol = __shfl_xor_sync(0xFFFFFFFFu, bl, o);
+        if (ov > bv || (ov == bv && oi < bid)) {
+          bv = ov;
+          bid = oi;
+          bl = ol;
+        }
+      }
+      const int kk = __shfl_sync(0xFFFFFFFFu, bk, bl);
+      V3 u = g;
+#pragma unroll
+      for (int k = 0; k < F_LOCAL; k++)
+        if (kk == k) u = lu[k];
+      SupU r;
+      r.val = bv;
+      r.id = bid;
+      r.u = v3(__shfl_sync(0xFFFFFFFFu, u.x, bl), __shfl_sync(0xFFFFFFFFu, u.y, bl),
+               __shfl_sync(0xFFFFFFFFu, u.z, bl));
+      return r;
+    };
+    // start from the candidate above v's radial plane found by (0)
+    SupU first;
+    first.val = s0.val;
+    first.id = s0.id;
+    first.u = vsub(v3(f.sx[s0.pos], f.sy[s0.pos], f.sz[s0.pos]), v);
+    V3 sep = w0;
+    const int r = gjk(local_sup, first, eps, &sep, &iters);
+    fs.iters += iters;
+    if (r == GJK_INSIDE) return 0;  // strictly inside the hull of other candidates
+    if (r == GJK_OUTSIDE) {
+      // (2) separated from the local set along sep: one global existence query
+      const double thr = mul(eps, sqrt_(vdot(sep, sep)));
+      const Sup c = support_query(f, P, sep, v, i, thr, true, stk, fs);
+      if (!(c.val > thr)) {
+        fs.certified++;
+        return 1;  // no candidate above the plane: extreme
+      }
     }
   }
-  *capped = 1;
+  // (3) global GJK, started from the candidate farthest along v - centre
+  const Sup s = support_query(f, P, w0, v, i, 0.0, false, stk, fs);
+  if (s.pos == 0xFFFFFFFFu) return 1;
+  // global GJK on U = {c - v : c != v} (branch-and-bound support queries)
+  auto global_sup = [&](V3 d) -> SupU {
+    const Sup q = support_query(f, P, d, v, i, 0.0, false, stk, fs);
+    SupU r;
+    r.val = q.val;
+    r.id = q.id;
+    r.u = q.pos == 0xFFFFFFFFu ? v3(0.0, 0.0, 0.0)
+                               : vsub(v3(f.sx[q.pos], f.sy[q.pos], f.sz[q.pos]), v);
+    return r;
+  };
+  SupU first;
+  first.val = s.val;
+  first.id = s.id;
+  first.u = vsub(v3(f.sx[s.pos], f.sy[s.pos], f.sz[s.pos]), v);
+  V3 sep;
+  iters = 0;
+  const int r = gjk(global_sup, first, eps, &sep, &iters);
+  fs.iters += iters;
+  if (r == GJK_INSIDE) return 0;
+  if (r == GJK_AMBIGUOUS) *amb = 1;
+  if (r == GJK_CAPPED) *capped = 1;
   return 1;
 }
 
-__global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_test(Workspace ws, FilterWs f) {
+__global__ void __launch_bounds__(F_TEST_BLOCK, 4) k_f_test(Workspace ws, FilterWs f) {
   __shared__ FilterParams sP;
   __shared__ FStack s_stk[F_TEST_BLOCK / 32];
   if (threadIdx.x == 0) sP = *f.fp;
@@ -766,6 +900,7 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_test(Workspace ws, Filter
   const uint32_t m = P.m;
   const double eps = ws.st->eps;
   const V3 ctr = v3(P.ctr[0], P.ctr[1], P.ctr[2]);
+  const V3 gsum = v3(P.gsum[0], P.gsum[1], P.gsum[2]);
   const int lane = threadIdx.x & 31;
   FStack& stk = s_stk[threadIdx.x >> 5];
   int amb_count = 0, cap_count = 0;
@@ -779,7 +914,8 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_test(Workspace ws, Filter
     if (ps >= m) break;
     const uint32_t i = __ldg(&f.sid[ps]);
     int keep = 1, amb = 0, capped = 0;
-    if (m > 4) keep = f_decide(f, P, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, eps, &amb, &capped, stk, fs);
+    if (m > 4)
+      keep = f_decide(f, P, ps, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, gsum, eps, &amb, &capped, stk, fs);
     if (lane == 0) {
       f.keep[i] = (uint8_t)keep;
       amb_count += amb;
