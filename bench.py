@@ -15,10 +15,13 @@ value     Mpoints/s = n * K / (device time of K hulls), input resident in HBM
 e2e       same metric through the public API with HOST (pinned) buffers:
           H2D copy of the points + hull + D2H of the vertex indices per step.
 roofline  the fused round kernel (k_round): algorithmic bytes of each launch
-          (R_d*(n_r + n_{r+1}), first split 8*dim*n +
-          R_d*n_1, R_d = 8*dim + 4) over its CUDA-event duration, measured in
-          an event-instrumented pass (launch mode 2) right after the timed
-          region; peak = MEASURED_PEAKS.json hbm_gbs.
+          over its CUDA-event duration, measured in an event-instrumented pass
+          (launch mode 2) right after the timed region; peak =
+          MEASURED_PEAKS.json hbm_gbs.  Bytes per launch (R_d = 8*dim + 4):
+          first split 8*dim*n (read only); round 1 8*dim*n + R_d*n_2 (it
+          re-reads the input instead of a materialised split); round r >= 2
+          R_d*(n_r + n_{r+1}).  whole_hull_frac uses SURVEY.md §8(d)'s
+          canonical B_alg (materialised split), which this design undercuts.
 cpu_baseline  the oracle (single-threaded C restatement of the reference
           drivers) on the same workload, rank 0, N=1 only.
 
@@ -343,7 +346,7 @@ def main():
     assert L.sh_fetch(ctx, ctypes.byref(res), sp) == 0
     assert int(res.h) == h and int(res.iterations) == rounds
     value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
-    launches_per_hull = 5 + 2 * rounds + (2 if dim == 3 else 0)
+    launches_per_hull = 5 + 2 * rounds + (8 if dim == 3 else 0)
 
     # ---------------- per-kernel pass (events after every launch)
     tr = P.trace(local)
@@ -359,7 +362,15 @@ def main():
     L.sh_set_launch_mode(ctx, 0)
     Rd = 8 * dim + 4
     n1 = int(tr[0, 0]) if len(tr) else 0
-    round_bytes = [8 * dim * n + Rd * n1] + [Rd * (int(a) + int(b)) for a, b, _, _ in tr]
+    # bytes each k_round launch must move in this design: the first split
+    # reads the input and writes nothing; round 1 re-reads the input (the
+    # split is re-derived on the fly) and writes its survivors; later rounds
+    # read and write R_d-byte records
+    round_bytes = [8 * dim * n]
+    for r, (a, b, _, _) in enumerate(tr):
+        round_bytes.append((8 * dim * n if r == 0 else Rd * int(a)) + Rd * int(b))
+    # SURVEY.md §8(d)'s canonical B_alg (materialised first split)
+    b_alg = 2 * 8 * dim * n + Rd * n1 + sum(Rd * (int(a) + int(b)) for a, b, _, _ in tr)
     best = None
     for kinds, ms in per:
         rt = ms[(kinds == KID_ROUND_FIRST) | (kinds == KID_ROUND)]
@@ -385,8 +396,9 @@ def main():
                     "algorithmic_bytes_per_launch": int(sum(round_bytes) / launches),
                     "avg_launch_ms": round(tot_round / launches, 4),
                     "share_of_kernel_time": round(tot_round / tot_all, 3),
-                    "whole_hull_frac": round(
-                        (sum(round_bytes) + 8 * dim * n) / (tot_ms / args.steps / 1e3) / 1e9 / peak, 4),
+                    "whole_hull_frac": round(b_alg / (tot_ms / args.steps / 1e3) / 1e9 / peak, 4),
+                    "whole_hull_b_alg_bytes": b_alg,
+                    "design_bytes_per_hull": sum(round_bytes) + 8 * dim * n,
                     "per_round_gbs": [round(float(b / (t / 1e3) / 1e9), 1) for b, t in
                                       zip(round_bytes, rt)],
                     "kernel_ms_by_kind": kernel_ms_by_kind}

@@ -193,6 +193,7 @@ struct Workspace {
   double* red;               // per block partial records
   uint32_t red_blocks;
   uint32_t round_grid;
+  uint32_t round1_grid;
   uint32_t book_grid;
   uint32_t max_tiles;     // round tiles at capacity
   cudaGraphConditionalHandle cond;

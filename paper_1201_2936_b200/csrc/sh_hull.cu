@@ -53,7 +53,7 @@ struct sh_ctx {
   size_t red_bytes = 0;
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[4];
-  int round_occ2 = 0, round_occ3 = 0, book_occ = 0;
+  int round_occ2 = 0, round_occ3 = 0, book_occ = 0, round1_occ2 = 0, round1_occ3 = 0;
   uint32_t last_n = 0;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
   // per-launch CUDA events (launch_mode 2): ev0[i] / ev1[i] right before /
@@ -181,6 +181,7 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
   CK(cudaMemset(w.st, 0, sizeof(DevState)));
   w.max_tiles = (uint32_t)max_tiles;
   w.round_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round_occ2 : c->round_occ3));
+  w.round1_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round1_occ2 : c->round1_occ3));
   w.book_grid = (uint32_t)(c->nsm * c->book_occ);
   c->dim = dim;
   c->cap_n = n;
@@ -215,7 +216,7 @@ template <int DIM>
 static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
   prof_begin(c, s);
-  k_round<DIM, false><<<ws.round_grid, RB, dsm, s>>>(ws);
+  k_round<DIM, MODE_NORMAL><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
   prof_begin(c, s);
@@ -243,9 +244,19 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
     prof_mark(c, s, KID_LINE_FAR);
   }
   prof_begin(c, s);
-  k_round<DIM, true><<<ws.round_grid, RB, dsm, s>>>(ws);
+  k_first_count<DIM><<<ws.red_blocks, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND_FIRST);
+  prof_begin(c, s);
+  k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
+  CK(cudaGetLastError());
+  prof_mark(c, s, KID_BOOK);
+  // round 1 re-reads the input and applies the first split on the fly, so
+  // the split's survivors are never written
+  prof_begin(c, s);
+  k_round<DIM, MODE_ROUND1><<<ws.round1_grid, RB, dsm, s>>>(ws);
+  CK(cudaGetLastError());
+  prof_mark(c, s, KID_ROUND);
   prof_begin(c, s);
   k_book<DIM><<<ws.book_grid, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
@@ -437,17 +448,26 @@ int sh_create(int device, sh_ctx** out) {
   sh_ctx* c = new sh_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  cudaFuncSetAttribute(k_round<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_round<2, MODE_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<2>::bytes());
-  cudaFuncSetAttribute(k_round<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_round<2, MODE_ROUND1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<2>::bytes());
-  cudaFuncSetAttribute(k_round<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_round<2, MODE_NORMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)RoundSmem<2>::bytes());
+  cudaFuncSetAttribute(k_round<3, MODE_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<3>::bytes());
-  cudaFuncSetAttribute(k_round<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_round<3, MODE_ROUND1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)RoundSmem<3>::bytes());
+  cudaFuncSetAttribute(k_round<3, MODE_NORMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<3>::bytes());
   int o2 = 0, o3 = 0, ob = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_round<2, false>, RB, RoundSmem<2>::bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_round<3, false>, RB, RoundSmem<3>::bytes());
+  int o2b = 0, o3b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_round<2, MODE_NORMAL>, RB, RoundSmem<2>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_round<3, MODE_NORMAL>, RB, RoundSmem<3>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2b, k_round<2, MODE_ROUND1>, RB, RoundSmem<2>::bytes());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3b, k_round<3, MODE_ROUND1>, RB, RoundSmem<3>::bytes());
+  c->round1_occ2 = std::max(1, o2b);
+  c->round1_occ3 = std::max(1, o3b);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
   c->round_occ2 = std::max(1, o2);
   c->round_occ3 = std::max(1, o3);

@@ -287,6 +287,144 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   }
 }
 
+// ------------------------------------------------------------------ K1
+// The first split (quickhull.py:200-222 / :346-364) as a counting pass:
+// per side, the number of points kept and the farthest one (largest
+// distance, lowest index among ties).  Nothing per point is written; round
+// 1 (k_round<MODE_ROUND1>) re-derives the split from the input.
+struct SideAgg {
+  uint32_t cnt[2];
+  unsigned long long hi[2];
+  uint32_t idx[2];
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(BLOCK) k_first_count(Workspace ws) {
+  DevState* st = ws.st;
+  const RoundParams rp = st->rp;
+  if (!rp.active || !rp.root) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->ctr_book = 0;
+    st->arrive_book = 0;
+    st->book_small = 1;
+  }
+  const uint32_t n = st->n;
+  const int64_t stride = st->stride;
+  const double pa0 = st->pa[0], pa1 = st->pa[1], pa2 = st->pa[2];
+  const double pb0 = st->pb[0], pb1 = st->pb[1];
+  const double n0 = st->nrm[0], n1 = st->nrm[1], n2 = st->nrm[2];
+  const double thr = st->thr_line;
+  const uint32_t imin = st->imin, imax = st->imax, ifar = (DIM == 3) ? st->ifar : 0xFFFFFFFFu;
+  SideAgg a;
+  a.cnt[0] = a.cnt[1] = 0;
+  a.hi[0] = a.hi[1] = 0ull;
+  a.idx[0] = a.idx[1] = 0xFFFFFFFFu;
+  double dmax = 0.0;
+  auto visit = [&](uint32_t i, double x, double y, double z) {
+    if (i == imin || i == imax || i == ifar) return;
+    int s;
+    double dn;
+    if (DIM == 2) {
+      const double d = cross2(pa0, pa1, pb0, pb1, x, y);
+      if (!(fabs(d) > thr)) return;
+      s = d < 0 ? 1 : 0;
+      dn = s ? -d : d;
+    } else {
+      const double nn[3] = {n0, n1, n2}, pp[3] = {pa0, pa1, pa2};
+      const double d = plane_dist(nn, pp, x, y, z);
+      dmax = fmax(dmax, fabs(d));
+      s = d < thr ? 1 : 0;
+      dn = s ? -d : d;
+    }
+    const unsigned long long k = ordered_bits(dn);
+    // indices arrive in increasing order per thread: strict > keeps the lowest
+    if (s == 0) {
+      a.cnt[0]++;
+      if (k > a.hi[0]) { a.hi[0] = k; a.idx[0] = i; }
+    } else {
+      a.cnt[1]++;
+      if (k > a.hi[1]) { a.hi[1] = k; a.idx[1] = i; }
+    }
+  };
+  const double* P[3] = {st->px, st->py, st->pz};
+  bool aligned = stride == 1;
+#pragma unroll
+  for (int k = 0; k < DIM; k++) aligned = aligned && ((reinterpret_cast<uintptr_t>(P[k]) & 15) == 0);
+  const uint32_t G = gridDim.x * BLOCK;
+  uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
+  if (aligned) {
+    const uint32_t npair = n / 2;
+    uint32_t pi = i;
+    for (; (uint64_t)pi + G < npair; pi += 2 * G) {  // two pairs in flight
+      double2 v[2][3];
+#pragma unroll
+      for (int u = 0; u < 2; u++)
+#pragma unroll
+        for (int k = 0; k < DIM; k++) v[u][k] = __ldcs(reinterpret_cast<const double2*>(P[k]) + pi + u * G);
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        visit(2 * (pi + u * G), v[u][0].x, v[u][1].x, DIM == 3 ? v[u][2].x : 0.0);
+        visit(2 * (pi + u * G) + 1, v[u][0].y, v[u][1].y, DIM == 3 ? v[u][2].y : 0.0);
+      }
+    }
+    for (; pi < npair; pi += G) {
+      double2 v[3];
+#pragma unroll
+      for (int k = 0; k < DIM; k++) v[k] = __ldcs(reinterpret_cast<const double2*>(P[k]) + pi);
+      visit(2 * pi, v[0].x, v[1].x, DIM == 3 ? v[2].x : 0.0);
+      visit(2 * pi + 1, v[0].y, v[1].y, DIM == 3 ? v[2].y : 0.0);
+    }
+    i = (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) ? n - 1 : n;  // odd tail
+  }
+  for (; i < n; i += G)
+    visit(i, ld_coord(P[0], stride, i), ld_coord(P[1], stride, i), DIM == 3 ? ld_coord(P[2], stride, i) : 0.0);
+  // warp + block reduction
+  __shared__ SideAgg s_w[WARPS];
+  __shared__ double s_d[WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+#pragma unroll
+    for (int s = 0; s < 2; s++) {
+      a.cnt[s] += __shfl_xor_sync(0xFFFFFFFFu, a.cnt[s], o);
+      const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, a.hi[s], o);
+      const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, a.idx[s], o);
+      if (oh > a.hi[s] || (oh == a.hi[s] && oi < a.idx[s])) {
+        a.hi[s] = oh;
+        a.idx[s] = oi;
+      }
+    }
+    dmax = fmax(dmax, __shfl_xor_sync(0xFFFFFFFFu, dmax, o));
+  }
+  if (lane == 0) {
+    s_w[warp] = a;
+    s_d[warp] = dmax;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int s = threadIdx.x;
+    uint32_t c = 0;
+    unsigned long long h = 0ull;
+    uint32_t x = 0xFFFFFFFFu;
+    for (int w = 0; w < WARPS; w++) {
+      c += s_w[w].cnt[s];
+      if (s_w[w].hi[s] > h || (s_w[w].hi[s] == h && s_w[w].idx[s] < x)) {
+        h = s_w[w].hi[s];
+        x = s_w[w].idx[s];
+      }
+    }
+    if (c) {
+      atomicAdd(&ws.cursor[0][s], c);  // root children (0, s): counts = cursor - 0
+      atomic_max_key(&ws.slot_key[s], h, x);
+    }
+  }
+  if (DIM == 3 && threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < WARPS; w++) m = fmax(m, s_d[w]);
+    if (m > 0.0) atomicMax((unsigned long long*)&st->dmax_bits, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
 // ------------------------------------------------------------------ bbox
 // Per-axis min / max of a point slice (sharded hulls all-reduce these to
 // the global Tolerance.effective, geometry.py:79-83).  Ordered-bits atomics

@@ -64,10 +64,13 @@ struct RoundShared {
   unsigned long long pend_hi[2][DIM];
   uint32_t pend_idx[2][DIM];
   // uniform tiles: per-warp totals / maxima, then per-warp output bases
-  uint32_t wtot[RB / 32][DIM];
-  unsigned long long whi[RB / 32][DIM];
-  uint32_t widx[RB / 32][DIM];
-  uint32_t boff[RB / 32][DIM];
+  uint32_t wtot[RB / 32][2 * DIM];
+  unsigned long long whi[RB / 32][2 * DIM];
+  uint32_t widx[RB / 32][2 * DIM];
+  uint32_t boff[RB / 32][2 * DIM];
+  // ROUND1: the block's running farthest keys of round 1's children
+  unsigned long long racc_hi[2 * DIM];
+  uint32_t racc_idx[2 * DIM];
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -146,9 +149,20 @@ __device__ __forceinline__ uint32_t win_search(const uint32_t* start, uint32_t n
   return lo;
 }
 
-template <int DIM, bool FIRST>
+// MODE_FIRST: the first split, counts and farthest keys only (no records
+//   are written: round 1 re-derives the split from the input).
+// MODE_ROUND1: round 1 fused with the first split: reads the input, drops
+//   what the first split drops, classifies the rest against the side's
+//   round-1 segment, writes round 1's survivors.
+// MODE_NORMAL: rounds 2.. over the records of the previous round.
+constexpr int MODE_FIRST = 0, MODE_ROUND1 = 1, MODE_NORMAL = 2;
+
+template <int DIM, int MODE>
 __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   constexpr int K = DIM;
+  constexpr bool FIRST = MODE == MODE_FIRST;
+  constexpr bool R1 = MODE == MODE_ROUND1;
+  constexpr bool INPUT = MODE != MODE_NORMAL;  // tiles over the caller's points
   DevState* st = ws.st;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ RoundShared<DIM> S;
@@ -156,12 +170,14 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
 
   const RoundParams rp = st->rp;
   if (!rp.active || (rp.root != 0) != FIRST) return;
+  if (R1 != (rp.round == 1) && !FIRST) return;
   if (blockIdx.x == 0 && tid == 0) {
     st->ctr_book = 0;  // K3's tile counter
     st->arrive_book = 0;
     st->book_small = (uint32_t)K * rp.nseg <= BOOK_SMALL ? 1u : 0u;
   }
-  const uint32_t n_live = rp.n_live, nseg = rp.nseg, cur = rp.cur;
+  const uint32_t nseg = rp.nseg, cur = rp.cur;
+  const uint32_t n_live = INPUT ? st->n : rp.n_live;  // positions the tiles cover
   const uint32_t num_tiles = (n_live + RTILE - 1) / RTILE;
   const uint32_t t0 = (uint32_t)(((uint64_t)num_tiles * blockIdx.x) / gridDim.x);
   const uint32_t t1 = (uint32_t)(((uint64_t)num_tiles * (blockIdx.x + 1)) / gridDim.x);
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   const double* py = st->py;
   const double* pz = st->pz;
   const int64_t pstride = st->stride;
-  if (FIRST) {
+  if (INPUT) {
 #pragma unroll
     for (int k = 0; k < 3; k++) {
       f_pa[k] = st->pa[k];
@@ -199,6 +215,10 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     if (DIM == 3) f_ifar = st->ifar;
   }
   double dmax_local = 0.0;
+  // ROUND1: segment of each first-split side (side 0 is segment 0 when it
+  // has survivors; the root children's counts are still in cursor[0])
+  uint32_t side_seg[2] = {0u, 0u};
+  if (R1) side_seg[1] = ws.cursor[0][0] ? 1u : 0u;
 
   auto stage_ptr = [&](uint32_t b) { return dsm + (size_t)b * RoundSmem<DIM>::stage_bytes(); };
 
@@ -225,13 +245,15 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   // segment (carried from the previous tile's window; a 32-ary search for a
   // block's first tile)
   auto load_window = [&](uint32_t t, uint32_t b) {
-    if (FIRST) {
+    if (INPUT) {
+      // FIRST: one root segment over the whole input; ROUND1: the round-1
+      // segments are the first split's sides, interleaved in input order
       if (lane == 0) {
         S.wlo[b] = 0;
-        S.wn[b] = 1;
+        S.wn[b] = FIRST ? 1u : nseg;
         S.wslow[b] = 0;
         S.wstart[b][0] = 0;
-        S.wstart[b][1] = n_live;
+        S.wstart[b][1] = FIRST ? n_live : 0u;
         S.wphys[b][0] = 0;
       }
       return;
@@ -290,7 +312,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     const double *gx = nullptr, *gy = nullptr, *gz = nullptr;
     const uint32_t* gi = nullptr;
     bool contig = false;
-    if (FIRST) {
+    if (INPUT) {
       contig = pstride == 1;
       gx = px + base;
       gy = py + base;
@@ -312,7 +334,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         cp_async16(&sx[RTILE + e], gy + e);
         if (DIM == 3) cp_async16(&sx[2 * RTILE + e], gz + e);
       }
-      if (!FIRST) {
+      if (!INPUT) {
         if (al16(gi)) {
 #pragma unroll
           for (int jq = 0; jq < RITEMS / 4; jq++) {
@@ -332,7 +354,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       const uint32_t i = j * RB + tid;
       const uint32_t q = base + i;
       uint32_t wfast = 0;
-      if (!FIRST && !contig && !slow) {
+      if (!INPUT && !contig && !slow) {
         // segment of q: the slot's first segment + the starts inside the slot
         const uint32_t wb = S.wslot[b][i >> 5];
         const uint32_t slot0 = base + (i & ~31u);
@@ -343,7 +365,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         wfast = wb + __popc(m & le);
       }
       if (i >= cnt) continue;
-      if (FIRST) {
+      if (INPUT) {
         const int64_t o = (int64_t)q * pstride;
         cp_async8(&sx[i], px + o);
         cp_async8(&sx[RTILE + i], py + o);
@@ -386,6 +408,10 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     S.pend_seg[tid] = NOKEY;
     S.pend_complete[tid] = 0;
   }
+  if (tid < 2 * K) {
+    S.racc_hi[tid] = 0ull;
+    S.racc_idx[tid] = 0xFFFFFFFFu;
+  }
   if (tid < 32) load_window(t0, 0);
   __syncthreads();
   issue_items(t0, 0);
@@ -414,19 +440,21 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     const bool uniform = S.wstart[b][1] >= tile_end;  // the whole tile lies in window segment 0
     uint32_t key[RITEMS], rank[RITEMS];
     unsigned long long khi_[RITEMS];
+    uint32_t wv[RITEMS];  // window segment of each item
     auto classify_item = [&](int j, bool uni, auto&& seg_of) {
       const uint32_t i = j * RB + tid;
       const uint32_t q = tile_begin + i;
       key[j] = NOKEY;
       rank[j] = 0;
       khi_[j] = 0;
+      wv[j] = 0;
       if (q >= tile_end) return;
       const double qx = sx[i], qy = sx[RTILE + i];
       const double qz = (DIM == 3) ? sx[2 * RTILE + i] : 0.0;
-      const uint32_t w = uni ? 0u : (uint32_t)sw[i];
+      uint32_t w = (uni || INPUT) ? 0u : (uint32_t)sw[i];
       double dn = 0.0;
       int s = -1;
-      if (FIRST) {
+      if (INPUT) {
         if (DIM == 2) {
           if (q != f_imin && q != f_imax) {
             // quickhull.py:202-211
@@ -440,16 +468,23 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
           if (q != f_imin && q != f_imax && q != f_ifar) {
             // quickhull.py:348-353
             double d = plane_dist(f_nrm, f_pa, qx, qy, qz);
-            dmax_local = fmax(dmax_local, fabs(d));
+            if (FIRST) dmax_local = fmax(dmax_local, fabs(d));
             s = d < f_thr ? 1 : 0;
             dn = s ? -d : d;  // face (pa, pc, pb) has normal -n exactly
           }
+        }
+        if (R1 && s >= 0) {
+          // round 1 on the survivors of the split: the side's segment
+          w = side_seg[s];
+          if constexpr (DIM == 2) s = classify2(seg_of(w), qx, qy, q, &dn);
+          else s = classify3(seg_of(w), qx, qy, qz, q, &dn);
         }
       } else {
         const uint32_t qi = si[i];
         if constexpr (DIM == 2) s = classify2(seg_of(w), qx, qy, qi, &dn);
         else s = classify3(seg_of(w), qx, qy, qz, qi, &dn);
       }
+      wv[j] = w;
       if (s >= 0) {
         key[j] = w * K + (uint32_t)s;
         // d > 0 for every live point except the 3D first split's near-plane
@@ -460,7 +495,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     };
     using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
     const SegT* segtab = reinterpret_cast<const SegT*>(ws.seg[cur]);
-    if (FIRST || (uniform && !slow)) {
+    if (FIRST || (uniform && !slow && !R1)) {
       SegT g0;
       if (!FIRST) g0 = *reinterpret_cast<const SegT*>(S.seg0[b]);  // staged with the window
 #pragma unroll
@@ -507,13 +542,16 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     };
     const int warp = tid >> 5;
 
-    if (!slow && uniform) {
-      // ---- one segment: ballots for ranks, register maxima, one claim per state
-      uint32_t wrun[K];
-      unsigned long long hm[K];
-      uint32_t im[K];
+    if (!slow && uniform && !R1) {
+      // ---- few keys (one segment's K states; ROUND1: both sides' states):
+      // ballots for ranks, register maxima, one claim per key
+      constexpr int NK = K;
+      const uint32_t nk = (uint32_t)K;
+      uint32_t wrun[NK];
+      unsigned long long hm[NK];
+      uint32_t im[NK];
 #pragma unroll
-      for (int s = 0; s < K; s++) {
+      for (int s = 0; s < NK; s++) {
         wrun[s] = 0;
         hm[s] = 0ull;
         im[s] = 0xFFFFFFFFu;
@@ -522,7 +560,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       for (int j = 0; j < RITEMS; j++) {
         uint32_t r = 0;
 #pragma unroll
-        for (int s = 0; s < K; s++) {
+        for (int s = 0; s < NK; s++) {
           const bool mine = key[j] == (uint32_t)s;
           const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
           r = mine ? wrun[s] + __popc(m & lanemask_lt()) : r;
@@ -533,7 +571,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         rank[j] = r;
       }
 #pragma unroll
-      for (int s = 0; s < K; s++) {
+      for (int s = 0; s < NK; s++) {
         const uint32_t mu = __reduce_max_sync(0xFFFFFFFFu, (uint32_t)(hm[s] >> 32));
         const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, ((uint32_t)(hm[s] >> 32) == mu) ? (uint32_t)hm[s] : 0u);
         hm[s] = ((unsigned long long)mu << 32) | ml;
@@ -542,15 +580,15 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
         const uint32_t i = j * RB + tid;
-        const uint32_t qi = FIRST ? tile_begin + i : si[i];
+        const uint32_t qi = INPUT ? tile_begin + i : si[i];
 #pragma unroll
-        for (int s = 0; s < K; s++) {
+        for (int s = 0; s < NK; s++) {
           const uint32_t c = (key[j] == (uint32_t)s && khi_[j] == hm[s]) ? qi : 0xFFFFFFFFu;
           im[s] = c < im[s] ? c : im[s];
         }
       }
 #pragma unroll
-      for (int s = 0; s < K; s++) {
+      for (int s = 0; s < NK; s++) {
         im[s] = __reduce_min_sync(0xFFFFFFFFu, im[s]);
         if (lane == 0) {
           S.wtot[warp][s] = wrun[s];
@@ -559,7 +597,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         }
       }
       __syncthreads();
-      if (tid < K) {
+      if (tid < nk) {
         const uint32_t s = tid;
         uint32_t tot = 0;
         unsigned long long hi = 0ull;
@@ -580,24 +618,33 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
           S.boff[w][s] = base;
           base += S.wtot[w][s];
         }
-        close_child(0, s, hi, idx);
+        if (R1) {
+          // round 1's children are interleaved over the whole input: fold
+          // into the block's running maxima, merged once per block below
+          if (hi > S.racc_hi[s] || (hi == S.racc_hi[s] && hi && idx < S.racc_idx[s])) {
+            S.racc_hi[s] = hi;
+            S.racc_idx[s] = idx;
+          }
+        } else {
+          close_child(0, s, hi, idx);
+        }
       }
       __syncthreads();
-      size_t wb[K];
+      size_t wb[NK];
 #pragma unroll
-      for (int s = 0; s < K; s++) wb[s] = (size_t)s * rcap + S.boff[warp][s];
+      for (int s = 0; s < NK; s++) wb[s] = (size_t)(s % K) * rcap + S.boff[warp][s];
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
-        if (key[j] == NOKEY) continue;
+        if (FIRST || key[j] == NOKEY) continue;  // the first split writes no records
         const uint32_t i = j * RB + tid;
         size_t dst = wb[0];
 #pragma unroll
-        for (int s = 1; s < K; s++) dst = key[j] == (uint32_t)s ? wb[s] : dst;
+        for (int s = 1; s < NK; s++) dst = key[j] == (uint32_t)s ? wb[s] : dst;
         dst += rank[j];
         outx[dst] = sx[i];
         outy[dst] = sx[RTILE + i];
         if (DIM == 3) outz[dst] = sx[2 * RTILE + i];
-        outi[dst] = FIRST ? (tile_begin + i) : si[i];
+        outi[dst] = INPUT ? (tile_begin + i) : si[i];
       }
       if (tid == 0 && !(has_next && S.wstart[b][nw] > tile_end)) S.pend_seg[pout] = NOKEY;
     } else if (!slow) {
@@ -608,7 +655,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       for (int j = 0; j < RITEMS; j++) {
         const uint32_t i = j * RB + tid;
         const bool valid = tile_begin + i < tile_end;
-        const uint32_t w = valid ? (uint32_t)sw[i] : 0u;
+        const uint32_t w = valid ? wv[j] : 0u;
         const uint32_t wmin = __reduce_min_sync(0xFFFFFFFFu, valid ? w : 0xFFFFu);
         const uint32_t wmax = __reduce_max_sync(0xFFFFFFFFu, valid ? w : 0u);
         const uint32_t hu = (uint32_t)(khi_[j] >> 32);
@@ -661,7 +708,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         if (key[j] == NOKEY) continue;
         const uint32_t i = j * RB + tid;
         const uint32_t kk = key[j];
-        const uint32_t qi = FIRST ? (tile_begin + i) : si[i];
+        const uint32_t qi = INPUT ? (tile_begin + i) : si[i];
         if ((uint32_t)(khi_[j] >> 32) == S.khh[kk] && (uint32_t)khi_[j] == S.khl[kk]) atomicMin(&S.kidx[kk], qi);
         const uint32_t s = kk % K;
         const size_t dst = (size_t)s * rcap + S.kbase[kk] + rank[j];
@@ -673,8 +720,17 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       __syncthreads();
       // ---- close, carry or merge every child of the tile
       for (uint32_t e = tid; e < ne; e += RB) {
-        close_child(e / K, e % K,
-                    S.kcnt[e] ? (((unsigned long long)S.khh[e] << 32) | S.khl[e]) : 0ull, S.kidx[e]);
+        const unsigned long long hk = S.kcnt[e] ? (((unsigned long long)S.khh[e] << 32) | S.khl[e]) : 0ull;
+        if (R1) {
+          // round 1's children are interleaved over the whole input: fold
+          // into the block's running maxima, merged once per block below
+          if (hk > S.racc_hi[e] || (hk == S.racc_hi[e] && hk && S.kidx[e] < S.racc_idx[e])) {
+            S.racc_hi[e] = hk;
+            S.racc_idx[e] = S.kidx[e];
+          }
+        } else {
+          close_child(e / K, e % K, hk, S.kidx[e]);
+        }
         S.kcnt[e] = 0;
         S.khh[e] = 0u;
         S.khl[e] = 0u;
@@ -707,6 +763,8 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     __syncthreads();  // stage b, window b and the child arrays are free
   }
 
+  if (R1 && tid < nseg * K && S.racc_hi[tid])
+    atomic_max_key(&ws.slot_key[tid], S.racc_hi[tid], S.racc_idx[tid]);
   if (FIRST && DIM == 3) {
     // coplanarity check input: max |d| of the first split (quickhull.py:349)
 #pragma unroll
