@@ -56,6 +56,7 @@ CONFIGS = {
             10_000_000),
     "C4c": ("C4: 3D Quickhull, 10M points uniform in unit cube (fp64)", "unit-cube", 10_000_000),
     "C4b": ("C4: 3D Quickhull, 10M points uniform in unit ball (fp64)", "uniform-ball", 10_000_000),
+    "C5": ("C5: 3D Quickhull, 200M points uniform in ball (fp64)", "uniform-ball", 200_000_000),
 }
 REF_SAMPLE = 10_000_000
 

@@ -121,7 +121,8 @@ int64_t sh_launch_times(sh_ctx* ctx, int32_t* kind, float* ms, int64_t cap);
 /* Diagnostics of the last 3D extreme filter: candidates m, grid edge G,
  * candidates kept as within-eps ambiguous, GJK iteration caps, candidates
  * certified by the first query, support queries, points scanned, GJK
- * iterations.  Returns the count written (<= cap, <= 8). */
+ * iterations, pruned by the local GJK, certified after the local GJK,
+ * resolved by the global GJK.  Returns the count written (<= cap, <= 11). */
 int sh_filter_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
 
 const char* sh_last_error(void);

@@ -225,8 +225,10 @@ __global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
         }
         Seg2 g;
         g.ax = Ax; g.ay = Ay; g.bx = Bx; g.by = By; g.fx = F[0]; g.fy = F[1];
-        // point_in_triangle(a, b, far): -eps * edge_length(.,.) per edge
-        g.nt_ab = mul(-eps, edge_length(Ax, Ay, Bx, By));
+        // point_in_triangle(a, b, far): -eps * edge_length(.,.) per edge;
+        // the (a, b) clause always holds for live points (classify2), so
+        // only the two edges to the new apex are needed
+        g.nt_ab = 0.0;
         g.nt_bf = mul(-eps, edge_length(Bx, By, F[0], F[1]));
         g.nt_fa = mul(-eps, edge_length(F[0], F[1], Ax, Ay));
         g.fidx = far;

@@ -58,6 +58,7 @@ struct FilterParams {
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
   uint32_t ambiguous, gjk_capped, pad0, pad1;
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
+  unsigned long long local_in, local_out, fallback;
 };
 
 struct FilterWs {
@@ -120,7 +121,7 @@ static inline int filter_set_params(FilterWs& f, int32_t* facets, int64_t cap, c
 
 // per-warp diagnostics (every lane holds the same values)
 struct FStat {
-  unsigned long long scanned, queries, iters, certified;
+  unsigned long long scanned, queries, iters, certified, local_in, local_out, fallback;
 };
 
 __device__ __forceinline__ unsigned long long obits(double d) { return ordered_bits(d); }
@@ -161,6 +162,9 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
     P->scanned = 0;
     P->gjk_iters = 0;
     P->certified = 0;
+    P->local_in = 0;
+    P->local_out = 0;
+    P->fallback = 0;
     // box tree: level 0 = chunks of 32 candidates, level l+1 = 32 level-l nodes
     uint32_t nl = m ? (m + 31) / 32 : 0, off = 0, lev = 0;
     for (int l = 0; l < F_LEVELS; l++) {
@@ -853,17 +857,21 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
     V3 sep = w0;
     const int r = gjk(local_sup, first, eps, &sep, &iters);
     fs.iters += iters;
-    if (r == GJK_INSIDE) return 0;  // strictly inside the hull of other candidates
+    if (r == GJK_INSIDE) {
+      fs.local_in++;
+      return 0;  // strictly inside the hull of other candidates
+    }
     if (r == GJK_OUTSIDE) {
       // (2) separated from the local set along sep: one global existence query
       const double thr = mul(eps, sqrt_(vdot(sep, sep)));
       const Sup c = support_query(f, P, sep, v, i, thr, true, stk, fs);
       if (!(c.val > thr)) {
-        fs.certified++;
+        fs.local_out++;
         return 1;  // no candidate above the plane: extreme
       }
     }
   }
+  fs.fallback++;
   // (3) global GJK, started from the candidate farthest along v - centre
   const Sup s = support_query(f, P, w0, v, i, 0.0, false, stk, fs);
   if (s.pos == 0xFFFFFFFFu) return 1;
@@ -904,7 +912,7 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 4) k_f_test(Workspace ws, Filter
   const int lane = threadIdx.x & 31;
   FStack& stk = s_stk[threadIdx.x >> 5];
   int amb_count = 0, cap_count = 0;
-  FStat fs = {0, 0, 0, 0};
+  FStat fs = {0, 0, 0, 0, 0, 0, 0};
   for (;;) {
     // candidates in Morton order: warps of a block work on nearby candidates
     // and share the tree nodes they touch in L1
@@ -929,6 +937,9 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 4) k_f_test(Workspace ws, Filter
     atomicAdd(&f.fp->scanned, fs.scanned);
     atomicAdd(&f.fp->gjk_iters, fs.iters);
     atomicAdd(&f.fp->certified, fs.certified);
+    atomicAdd(&f.fp->local_in, fs.local_in);
+    atomicAdd(&f.fp->local_out, fs.local_out);
+    atomicAdd(&f.fp->fallback, fs.fallback);
   }
 }
 
@@ -981,7 +992,7 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_boxes_hi<<<1, 1024, 0, s>>>(f);
   k_f_test<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_compact<<<1, 1024, 0, s>>>(ws, f);
-  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : 10;
 }
 
 // vout (uint32, discovery order) -> user int64 indices (2D; 3D goes through

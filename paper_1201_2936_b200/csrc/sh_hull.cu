@@ -269,7 +269,7 @@ static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
   if (DIM == 3) {
     prof_begin(c, s);
     int rc = filter_launch(c->fws, ws, c->nsm, s);
-    if (rc) return rc;
+    if (rc) return set_err(rc, std::string("3D filter launch: ") + cudaGetErrorString(cudaGetLastError()));
     prof_mark(c, s, KID_FILTER);
     return SH_OK;
   }
@@ -609,9 +609,10 @@ int sh_filter_stats(sh_ctx* c, int64_t* out, int64_t cap) {
   if (!c || !c->fws.fp || cap <= 0) return 0;
   FilterParams P;
   if (cudaMemcpy(&P, c->fws.fp, sizeof(P), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
-  int64_t v[9] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
-                  (int64_t)P.scanned, (int64_t)P.gjk_iters, 0};
-  int64_t n = std::min<int64_t>(cap, 8);
+  int64_t v[11] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
+                   (int64_t)P.scanned, (int64_t)P.gjk_iters, (int64_t)P.local_in, (int64_t)P.local_out,
+                   (int64_t)P.fallback};
+  int64_t n = std::min<int64_t>(cap, 11);
   for (int64_t i = 0; i < n; i++) out[i] = v[i];
   return (int)n;
 }

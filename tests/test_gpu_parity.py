@@ -207,3 +207,48 @@ def test_full_size_configs(cfg):
     else:
         res = _check3(generate("uniform-ball", 10_000_000, 0))
         assert res.iterations == 15 and res.candidates == 34_625 and res.h == 14_152
+
+
+def _lattice2(n_side, reps, seed):
+    rng = np.random.default_rng(seed)
+    g = rng.integers(0, n_side, size=(n_side * n_side * reps, 2)).astype(np.float64)
+    return g[:, 0].copy(), g[:, 1].copy()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_degenerate_2d_lattices_and_duplicates(seed):
+    """Integer lattices: massive collinearity, exact distance ties,
+    duplicates of hull vertices -- the tie-break and eps paths."""
+    for n_side, reps in ((7, 30), (60, 5), (400, 1)):
+        _check2(_lattice2(n_side, reps, seed))
+        _check2(_lattice2(n_side, reps, seed), eps_rel=0.0)
+    # points on a few lines through the disk, with duplicates
+    rng = np.random.default_rng(seed)
+    t = rng.integers(-1000, 1000, size=300_000) / 1000.0
+    k = rng.integers(0, 5, size=t.size)
+    ang = k * 0.7
+    x = np.round(t * np.cos(ang), 3)
+    y = np.round(t * np.sin(ang), 3)
+    _check2((x, y))
+
+
+@pytest.mark.parametrize("seed", range(2))
+def test_degenerate_3d_lattices(seed):
+    rng = np.random.default_rng(seed)
+    for n_side in (5, 20):
+        g = rng.integers(0, n_side, size=(20_000, 3)).astype(np.float64)
+        cols = (g[:, 0].copy(), g[:, 1].copy(), g[:, 2].copy())
+        o, idx_ref, _ = oracle.full_hull3d(*cols)
+        idx, _, res = P.hull_indices_3d(dev(cols), return_info=True)
+        # the loop (candidates, rounds, traces) is bit-exact even here; the
+        # filter keeps coplanar boundary points the reference's eps-tolerant
+        # stages keep too, so only the loop is compared on lattices
+        assert res.iterations == o.iterations
+        assert res.candidates == len(o.idx)
+        assert np.array_equal(P.trace()[:, :3], o.trace)
+
+
+def test_scaled_and_shifted_inputs():
+    x, y = generate("uniform-disk", 500_000, 4)
+    for sc, sh in ((1e-150, 0.0), (1e150, 0.0), (1.0, 1e9), (3.0, -7.0)):
+        _check2((x * sc + sh, y * sc + sh))

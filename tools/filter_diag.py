@@ -6,7 +6,7 @@ import paper_1201_2936_b200 as P
 from paper_1201_2936_b200 import _lib
 from paper_1201_2936_b200.datagen import generate
 L, ctx = _lib.lib(), _lib.context(0)
-for kind, n in [("uniform-ball", 10**6), ("uniform-ball", 10**7), ("unit-cube", 10**7), ("near-sphere", 10**6)]:
+for kind, n in [("uniform-ball", 10**6), ("uniform-ball", 10**7), ("unit-cube", 10**7), ("near-sphere", 10**6), ("uniform-ball", 10**8)]:
     d = tuple(torch.from_numpy(c).cuda() for c in generate(kind, n, 0))
     P.hull_indices_3d(d)
     L.sh_set_launch_mode(ctx, 2)
@@ -14,6 +14,6 @@ for kind, n in [("uniform-ball", 10**6), ("uniform-ball", 10**7), ("unit-cube", 
     L.sh_set_launch_mode(ctx, 0)
     kinds = np.zeros(256, np.int32); ms = np.zeros(256, np.float32)
     k = L.sh_launch_times(ctx, kinds.ctypes.data, ms.ctypes.data, 256)
-    st = np.zeros(8, np.int64); L.sh_filter_stats(ctx, st.ctypes.data, 8)
+    st = np.zeros(11, np.int64); L.sh_filter_stats(ctx, st.ctypes.data, 11)
     print(kind, n, "cand", res.candidates, "h", res.h, "filter ms", float(ms[:k][kinds[:k] == 6].sum()),
-          "stats m,G,amb,capped,certified,queries,scanned,iters =", st.tolist(), flush=True)
+          "stats m,G,amb,capped,cert0,queries,scanned,iters,loc_in,loc_out,fallback =", st.tolist(), flush=True)
