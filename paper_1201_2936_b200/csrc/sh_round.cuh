@@ -412,6 +412,13 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     S.racc_hi[tid] = 0ull;
     S.racc_idx[tid] = 0xFFFFFFFFu;
   }
+  if (R1) {
+    // round 1's (at most two) segment tables, constant for the whole launch
+    using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ws.seg[cur]);
+    for (uint32_t k = tid; k < nseg * (sizeof(SegT) / 8); k += RB)
+      S.seg0[k / (sizeof(SegT) / 8)][k % (sizeof(SegT) / 8)] = src[k];
+  }
   if (tid < 32) load_window(t0, 0);
   __syncthreads();
   issue_items(t0, 0);
@@ -500,6 +507,10 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       if (!FIRST) g0 = *reinterpret_cast<const SegT*>(S.seg0[b]);  // staged with the window
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) classify_item(j, true, [&](uint32_t) -> const SegT& { return g0; });
+    } else if (R1) {
+#pragma unroll
+      for (int j = 0; j < RITEMS; j++)
+        classify_item(j, false, [&](uint32_t w) -> const SegT& { return *reinterpret_cast<const SegT*>(S.seg0[w]); });
     } else {
 #pragma unroll
       for (int j = 0; j < RITEMS; j++)
