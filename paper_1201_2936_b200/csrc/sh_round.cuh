@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       __syncwarp();
       // one binary search per 32-point slot (all slots at once, one per lane)
       const uint32_t q = base + lane * 32;
-      S.wslot[b][lane] = q < n_live ? win_search(S.wstart[b], nw, q) : 0u;
+      if (lane < RTILE / 32) S.wslot[b][lane] = q < n_live ? win_search(S.wstart[b], nw, q) : 0u;
     }
     {
       using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
