@@ -34,7 +34,7 @@ struct BookShared {
 };
 
 template <int DIM>
-__global__ void __launch_bounds__(BLOCK) k_book(Workspace ws) {
+__global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) {
   constexpr int K = DIM;
   DevState* st = ws.st;
   __shared__ BookShared sb;

@@ -53,7 +53,7 @@ struct sh_ctx {
   size_t red_bytes = 0;
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[4];
-  int round_occ2 = 0, round_occ3 = 0, book_occ = 0, round1_occ2 = 0, round1_occ3 = 0;
+  int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0, round1_occ2 = 0, round1_occ3 = 0;
   uint32_t last_n = 0;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
   // per-launch CUDA events (launch_mode 2): ev0[i] / ev1[i] right before /
@@ -182,7 +182,7 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
   w.max_tiles = (uint32_t)max_tiles;
   w.round_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round_occ2 : c->round_occ3));
   w.round1_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round1_occ2 : c->round1_occ3));
-  w.book_grid = (uint32_t)(c->nsm * c->book_occ);
+  w.book_grid = (uint32_t)(c->nsm * (dim == 2 ? c->book_occ2 : c->book_occ3));
   c->dim = dim;
   c->cap_n = n;
   c->segcap = segcap;
@@ -468,10 +468,13 @@ int sh_create(int device, sh_ctx** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3b, k_round<3, MODE_ROUND1>, RB, RoundSmem<3>::bytes());
   c->round1_occ2 = std::max(1, o2b);
   c->round1_occ3 = std::max(1, o3b);
+  int ob2 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob2, k_book<2>, BLOCK, 0);
   c->round_occ2 = std::max(1, o2);
   c->round_occ3 = std::max(1, o3);
-  c->book_occ = std::max(1, std::min(ob, 4));
+  c->book_occ3 = std::max(1, std::min(ob, 4));
+  c->book_occ2 = std::max(1, std::min(ob2, 4));
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     delete c;
