@@ -448,14 +448,10 @@ int sh_create(int device, sh_ctx** out) {
   sh_ctx* c = new sh_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  cudaFuncSetAttribute(k_round<2, MODE_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)RoundSmem<2>::bytes());
   cudaFuncSetAttribute(k_round<2, MODE_ROUND1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<2>::bytes());
   cudaFuncSetAttribute(k_round<2, MODE_NORMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<2>::bytes());
-  cudaFuncSetAttribute(k_round<3, MODE_FIRST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)RoundSmem<3>::bytes());
   cudaFuncSetAttribute(k_round<3, MODE_ROUND1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<3>::bytes());
   cudaFuncSetAttribute(k_round<3, MODE_NORMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,

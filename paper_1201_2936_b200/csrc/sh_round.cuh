@@ -1,12 +1,14 @@
-// K1/K2: the fused Quickhull round kernel.
+// K2: the fused Quickhull round kernel.
 //
 // One launch processes one whole round over all segments at once, reading
 // every live record once and writing every survivor once
-// (quickhull.py:229-266 / :372-437; the first split :200-222 / :346-364 is
-// the FIRST instantiation).
+// (quickhull.py:229-266 / :372-437).  Round 1 is fused with the first split
+// (quickhull.py:200-222 / :346-364): it reads the input and re-derives each
+// point's side, so the split's survivors are never materialised
+// (MODE_ROUND1; k_first_count only counts the split and finds its apexes).
 //
 // Work split: persistent blocks, each owning a static contiguous range of
-// 1024-point tiles.  Tiles are independent -- there is no tile-to-tile
+// 512-point tiles.  Tiles are independent -- there is no tile-to-tile
 // prefix chain: every child (parent segment p, state s) owns a disjoint
 // region of output stream s starting at p's start, and survivors claim
 // positions in it with one shared-memory atomic per warp and one global
@@ -149,18 +151,16 @@ __device__ __forceinline__ uint32_t win_search(const uint32_t* start, uint32_t n
   return lo;
 }
 
-// MODE_FIRST: the first split, counts and farthest keys only (no records
-//   are written: round 1 re-derives the split from the input).
+// (The first split itself is a read-only counting pass, k_first_count.)
 // MODE_ROUND1: round 1 fused with the first split: reads the input, drops
 //   what the first split drops, classifies the rest against the side's
 //   round-1 segment, writes round 1's survivors.
 // MODE_NORMAL: rounds 2.. over the records of the previous round.
-constexpr int MODE_FIRST = 0, MODE_ROUND1 = 1, MODE_NORMAL = 2;
+constexpr int MODE_ROUND1 = 1, MODE_NORMAL = 2;
 
 template <int DIM, int MODE>
 __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   constexpr int K = DIM;
-  constexpr bool FIRST = MODE == MODE_FIRST;
   constexpr bool R1 = MODE == MODE_ROUND1;
   constexpr bool INPUT = MODE != MODE_NORMAL;  // tiles over the caller's points
   DevState* st = ws.st;
@@ -169,8 +169,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   const int tid = threadIdx.x, lane = tid & 31;
 
   const RoundParams rp = st->rp;
-  if (!rp.active || (rp.root != 0) != FIRST) return;
-  if (R1 != (rp.round == 1) && !FIRST) return;
+  if (!rp.active || rp.root || R1 != (rp.round == 1)) return;
   if (blockIdx.x == 0 && tid == 0) {
     st->ctr_book = 0;  // K3's tile counter
     st->arrive_book = 0;
@@ -214,7 +213,6 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     f_imax = st->imax;
     if (DIM == 3) f_ifar = st->ifar;
   }
-  double dmax_local = 0.0;
   // ROUND1: segment of each first-split side (side 0 is segment 0 when it
   // has survivors; the root children's counts are still in cursor[0])
   uint32_t side_seg[2] = {0u, 0u};
@@ -246,14 +244,14 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
   // block's first tile)
   auto load_window = [&](uint32_t t, uint32_t b) {
     if (INPUT) {
-      // FIRST: one root segment over the whole input; ROUND1: the round-1
-      // segments are the first split's sides, interleaved in input order
+      // ROUND1: the round-1 segments are the first split's sides,
+      // interleaved in input order
       if (lane == 0) {
         S.wlo[b] = 0;
-        S.wn[b] = FIRST ? 1u : nseg;
+        S.wn[b] = nseg;
         S.wslow[b] = 0;
         S.wstart[b][0] = 0;
-        S.wstart[b][1] = FIRST ? n_live : 0u;
+        S.wstart[b][1] = 0;
         S.wphys[b][0] = 0;
       }
       return;
@@ -475,7 +473,6 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
           if (q != f_imin && q != f_imax && q != f_ifar) {
             // quickhull.py:348-353
             double d = plane_dist(f_nrm, f_pa, qx, qy, qz);
-            if (FIRST) dmax_local = fmax(dmax_local, fabs(d));
             s = d < f_thr ? 1 : 0;
             dn = s ? -d : d;  // face (pa, pc, pb) has normal -n exactly
           }
@@ -494,17 +491,15 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       wv[j] = w;
       if (s >= 0) {
         key[j] = w * K + (uint32_t)s;
-        // d > 0 for every live point except the 3D first split's near-plane
-        // side-0 points, so the raw bits already order correctly there
-        khi_[j] = (FIRST && DIM == 3) ? ordered_bits(dn)
-                                      : (unsigned long long)__double_as_longlong(dn) | 0x8000000000000000ull;
+        // d > 0 for every live point (see classify2), so the raw bits order
+        // like ordered_bits(d)
+        khi_[j] = (unsigned long long)__double_as_longlong(dn) | 0x8000000000000000ull;
       }
     };
     using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
     const SegT* segtab = reinterpret_cast<const SegT*>(ws.seg[cur]);
-    if (FIRST || (uniform && !slow && !R1)) {
-      SegT g0;
-      if (!FIRST) g0 = *reinterpret_cast<const SegT*>(S.seg0[b]);  // staged with the window
+    if (uniform && !slow && !R1) {
+      const SegT g0 = *reinterpret_cast<const SegT*>(S.seg0[b]);  // staged with the window
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) classify_item(j, true, [&](uint32_t) -> const SegT& { return g0; });
     } else if (R1) {
@@ -646,7 +641,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
       for (int s = 0; s < NK; s++) wb[s] = (size_t)(s % K) * rcap + S.boff[warp][s];
 #pragma unroll
       for (int j = 0; j < RITEMS; j++) {
-        if (FIRST || key[j] == NOKEY) continue;  // the first split writes no records
+        if (key[j] == NOKEY) continue;
         const uint32_t i = j * RB + tid;
         size_t dst = wb[0];
 #pragma unroll
@@ -776,13 +771,6 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
 
   if (R1 && tid < nseg * K && S.racc_hi[tid])
     atomic_max_key(&ws.slot_key[tid], S.racc_hi[tid], S.racc_idx[tid]);
-  if (FIRST && DIM == 3) {
-    // coplanarity check input: max |d| of the first split (quickhull.py:349)
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) dmax_local = fmax(dmax_local, __shfl_xor_sync(0xFFFFFFFFu, dmax_local, m));
-    if (lane == 0 && dmax_local > 0.0)
-      atomicMax((unsigned long long*)&st->dmax_bits, (unsigned long long)__double_as_longlong(dmax_local));
-  }
 }
 
 }  // namespace sh
