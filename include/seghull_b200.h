@@ -125,6 +125,30 @@ int64_t sh_launch_times(sh_ctx* ctx, int32_t* kind, float* ms, int64_t cap);
  * resolved by the global GJK.  Returns the count written (<= cap, <= 11). */
 int sh_filter_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
 
+/* ---- framework primitives (device arrays) ----
+ * Replace segments.segmented_scan (segments.py:201-234), flag_permute
+ * (primitives.py:91-117), compact (:120-148) and scatter (:151-176).
+ * heads: uint8 segment-head flags (element 0 is always a head).
+ * op: 0 sum (int64 only), 1 max, 2 min.  values/out: int64, or fp64 when
+ * is_f64 (max/min; -0.0 is canonicalised to +0.0 as segments.py:197). */
+int sh_segmented_scan(sh_ctx* ctx, const void* values, int is_f64, const uint8_t* heads, int64_t n, int op,
+                      int backward, int exclusive, void* out, void* stream);
+/* Stable in-segment grouping by state f in [0, k): destination p (int64,
+ * a bijection within each segment) and new heads (uint8, length n). */
+int sh_flag_permute(sh_ctx* ctx, const int64_t* f, const uint8_t* heads, int64_t n, int64_t k, int64_t* p,
+                    uint8_t* heads_out, void* stream);
+/* Keep-mask compaction: p = exclusive count of kept elements (int64),
+ * *out_len (host) = number kept, heads_out (uint8, capacity n, first
+ * *out_len written) = each surviving segment's head at its first kept
+ * element.  Synchronises the stream (the output length is returned). */
+int sh_compact(sh_ctx* ctx, const uint8_t* b, const uint8_t* heads, int64_t n, int64_t* p, int64_t* out_len,
+               uint8_t* heads_out, void* stream);
+/* out[p[i]] = data[i] (rows of row_bytes) for live i (live may be NULL);
+ * SH_CONTRACT on colliding or out-of-range destinations (checked before any
+ * write).  Synchronises the stream. */
+int sh_scatter(sh_ctx* ctx, const void* data, int64_t row_bytes, const int64_t* p, const uint8_t* live,
+               int64_t n, int64_t out_len, void* out, void* stream);
+
 const char* sh_last_error(void);
 const char* sh_version(void);
 

@@ -2,18 +2,25 @@
 entry points of the reference package ``seghull``.
 
 Drop-in names: quickhull_2d, quickhull_3d, HullResult, PointSet, Tolerance,
-ContractViolation, EmptyInputError, DegenerateInputError.  Device-tensor
-variants: hull_indices_2d, hull_indices_3d.  See DESIGN.md.
+ContractViolation, EmptyInputError, DegenerateInputError; the framework
+primitives segmented_scan, ScanSpec, flag_permute, compact, scatter,
+PermutationMap, head_index_broadcast, segment_ids, reduce_broadcast (GPU ops).
+Device-tensor variants: hull_indices_2d, hull_indices_3d; multi-GPU:
+paper_1201_2936_b200.sharded.  See DESIGN.md.
 """
 
 from .errors import ContractViolation, DegenerateInputError, EmptyInputError
 from .geometry import PointSet, Tolerance
+from .primitives import (PermutationMap, ScanSpec, compact, flag_permute, head_index_broadcast,
+                         reduce_broadcast, scatter, segment_ids, segmented_scan)
 from .quickhull import (HullResult, hull_indices_2d, hull_indices_3d, quickhull_2d, quickhull_3d,
                         trace)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ContractViolation", "DegenerateInputError", "EmptyInputError", "HullResult", "PointSet",
-    "Tolerance", "hull_indices_2d", "hull_indices_3d", "quickhull_2d", "quickhull_3d", "trace",
+    "ContractViolation", "DegenerateInputError", "EmptyInputError", "HullResult", "PermutationMap",
+    "PointSet", "ScanSpec", "Tolerance", "compact", "flag_permute", "head_index_broadcast",
+    "hull_indices_2d", "hull_indices_3d", "quickhull_2d", "quickhull_3d", "reduce_broadcast",
+    "scatter", "segment_ids", "segmented_scan", "trace",
 ]

@@ -22,6 +22,7 @@
 #include "sh_book.cuh"
 #include "sh_filter3.cuh"
 #include "sh_kernels.cuh"
+#include "sh_prims.cuh"
 #include "sh_round.cuh"
 
 using namespace sh;
@@ -437,6 +438,28 @@ static int hull_sync(sh_ctx* c, const double* x, const double* y, const double* 
   return set_err(SH_NOMEM, "segment table capacity retries exhausted");
 }
 
+// ---------------------------------------------------------- primitives
+static PsView ps_view(const void* vals, const uint8_t* heads, int64_t n, int backward) {
+  PsView v;
+  memset(&v, 0, sizeof(v));
+  v.vals = vals;
+  v.heads = heads;
+  v.n = n;
+  v.backward = backward;
+  return v;
+}
+
+template <class T>
+static int ps_launch(PsView v, int op, int exclusive, T* out, cudaStream_t s) {
+  const int64_t ntiles = (v.n + PS_TILE - 1) / PS_TILE;
+  PsAgg<T>* scratch = nullptr;
+  CK(cudaMallocAsync((void**)&scratch, (size_t)(ntiles + 1) * sizeof(PsAgg<T>), s));
+  int rc = ps_run<T>(v, op, exclusive, out, scratch, s);
+  cudaFreeAsync(scratch, s);
+  if (rc) return set_err(SH_CUDA, std::string("segmented scan launch: ") + cudaGetErrorString(cudaGetLastError()));
+  return SH_OK;
+}
+
 // ---------------------------------------------------------------- C ABI
 extern "C" {
 
@@ -601,6 +624,132 @@ int sh_bbox(sh_ctx* c, const double* x, const double* y, const double* z, int64_
   k_bbox<<<c->nsm * 8, BLOCK, 0, s>>>(x, y, dim == 3 ? z : y, stride, (uint32_t)n, dim, c->bbox_bits);
   k_bbox_final<<<1, 32, 0, s>>>(c->bbox_bits, out, dim);
   CK(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_segmented_scan(sh_ctx* c, const void* values, int is_f64, const uint8_t* heads, int64_t n, int op,
+                      int backward, int exclusive, void* out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (n < 0 || (n > 0 && (!values || !heads || !out)) || op < 0 || op > 2 || (is_f64 && op == PS_SUM))
+    return set_err(SH_CONTRACT, "bad segmented scan arguments");
+  if (n == 0) return SH_OK;
+  CK(cudaSetDevice(c->device));
+  PsView v = ps_view(values, heads, n, backward);
+  cudaStream_t s = (cudaStream_t)stream;
+  return is_f64 ? ps_launch<double>(v, op, exclusive, (double*)out, s)
+                : ps_launch<long long>(v, op, exclusive, (long long*)out, s);
+}
+
+int sh_flag_permute(sh_ctx* c, const int64_t* f, const uint8_t* heads, int64_t n, int64_t k, int64_t* p,
+                    uint8_t* heads_out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (n < 0 || k < 1 || (n > 0 && (!f || !heads || !p || !heads_out)))
+    return set_err(SH_CONTRACT, "bad flag permute arguments");
+  if (n == 0) return SH_OK;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *seg = nullptr, *rank = nullptr, *seg_start = nullptr;
+  unsigned long long* counts = nullptr;
+  CK(cudaMallocAsync((void**)&seg, n * 8, s));
+  CK(cudaMallocAsync((void**)&rank, n * 8, s));
+  CK(cudaMallocAsync((void**)&seg_start, n * 8, s));
+  CK(cudaMallocAsync((void**)&counts, (size_t)n * k * 8, s));
+  CK(cudaMemsetAsync(counts, 0, (size_t)n * k * 8, s));
+  // segment id = inclusive count of heads - 1 (element 0 always heads)
+  PsView hv = ps_view(nullptr, nullptr, n, 0);
+  hv.u8 = heads;
+  hv.force0 = 1;
+  int rc = ps_launch<long long>(hv, PS_SUM, 0, (long long*)seg, s);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + BLOCK - 1) / BLOCK, 65535);
+  if (!rc) {
+    k_fp_subone<<<grid, BLOCK, 0, s>>>(seg, n);
+    k_fp_counts<<<grid, BLOCK, 0, s>>>(f, seg, n, k, heads, counts, seg_start);
+  }
+  // stable in-segment rank per state: exclusive segmented count of state j
+  for (int64_t j = 0; j < k && !rc; j++) {
+    PsView sv = ps_view(nullptr, heads, n, 0);
+    sv.states = f;
+    sv.state = j;
+    rc = ps_launch<long long>(sv, PS_SUM, 1, (long long*)rank, s);
+  }
+  if (!rc) {
+    k_fp_assemble<<<grid, BLOCK, 0, s>>>(f, seg, rank, n, k, counts, seg_start, p, heads_out);
+    k_fp_heads<<<grid, BLOCK, 0, s>>>(n, k, counts, seg_start, heads_out);
+  }
+  cudaFreeAsync(seg, s);
+  cudaFreeAsync(rank, s);
+  cudaFreeAsync(seg_start, s);
+  cudaFreeAsync(counts, s);
+  if (rc) return rc;
+  CK(cudaPeekAtLastError());
+  return SH_OK;
+}
+
+int sh_compact(sh_ctx* c, const uint8_t* b, const uint8_t* heads, int64_t n, int64_t* p, int64_t* out_len,
+               uint8_t* heads_out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (n < 0 || !out_len || (n > 0 && (!b || !heads || !p || !heads_out)))
+    return set_err(SH_CONTRACT, "bad compact arguments");
+  *out_len = 0;
+  if (n == 0) return SH_OK;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  // p = exclusive count of kept elements (one segment)
+  PsView kv = ps_view(nullptr, nullptr, n, 0);
+  kv.u8 = b;
+  int rc = ps_launch<long long>(kv, PS_SUM, 1, (long long*)p, s);
+  if (rc) return rc;
+  int64_t last_p = 0;
+  uint8_t last_b = 0;
+  CK(cudaMemcpyAsync(&last_p, p + n - 1, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&last_b, b + n - 1, 1, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *out_len = last_p + (last_b ? 1 : 0);
+  // each head moves to the first kept destination at or after it
+  // (backward segmented min scan of kept destinations, primitives.py:141-146)
+  int64_t* firsts = nullptr;
+  CK(cudaMallocAsync((void**)&firsts, n * 8, s));
+  PsView mv = ps_view(nullptr, heads, n, 1);
+  mv.keep = b;
+  mv.mvals = p;
+  rc = ps_launch<long long>(mv, PS_MIN, 0, (long long*)firsts, s);
+  if (!rc && *out_len > 0) {
+    CK(cudaMemsetAsync(heads_out, 0, *out_len, s));
+    const unsigned grid = (unsigned)std::min<int64_t>((n + BLOCK - 1) / BLOCK, 65535);
+    k_cp_heads<<<grid, BLOCK, 0, s>>>(firsts, heads, n, heads_out);
+  }
+  cudaFreeAsync(firsts, s);
+  if (rc) return rc;
+  CK(cudaPeekAtLastError());
+  return SH_OK;
+}
+
+int sh_scatter(sh_ctx* c, const void* data, int64_t row_bytes, const int64_t* p, const uint8_t* live, int64_t n,
+               int64_t out_len, void* out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (n < 0 || out_len < 0 || row_bytes < 1 || (n > 0 && (!data || !p)) || (out_len > 0 && !out))
+    return set_err(SH_CONTRACT, "bad scatter arguments");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (out_len > 0) CK(cudaMemsetAsync(out, 0, (size_t)out_len * row_bytes, s));
+  if (n == 0) return SH_OK;
+  unsigned int* hits = nullptr;
+  unsigned long long* err = nullptr;
+  CK(cudaMallocAsync((void**)&hits, (size_t)(out_len + 1) * 4, s));
+  CK(cudaMallocAsync((void**)&err, 16, s));
+  CK(cudaMemsetAsync(hits, 0, (size_t)(out_len + 1) * 4, s));
+  CK(cudaMemsetAsync(err, 0, 16, s));
+  const unsigned grid = (unsigned)std::min<int64_t>((n + BLOCK - 1) / BLOCK, 65535);
+  k_scatter_check<<<grid, BLOCK, 0, s>>>(p, live, n, out_len, hits, err);
+  unsigned long long herr[2] = {0, 0};
+  CK(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFreeAsync(hits, s);
+  cudaFreeAsync(err, s);
+  if (herr[1]) return set_err(SH_CONTRACT, "map destination out of range");
+  if (herr[0]) return set_err(SH_CONTRACT, "map destinations collide");
+  k_scatter<<<grid, BLOCK, 0, s>>>((const unsigned char*)data, p, live, n, row_bytes, (unsigned char*)out);
+  CK(cudaPeekAtLastError());
   return SH_OK;
 }
 
