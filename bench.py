@@ -347,7 +347,9 @@ def main():
     assert L.sh_fetch(ctx, ctypes.byref(res), sp) == 0
     assert int(res.h) == h and int(res.iterations) == rounds
     value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
-    launches_per_hull = 5 + 2 * rounds + (8 if dim == 3 else 0)
+    # init, first reduce, first-split count, book, then (round, book) per
+    # round, then output (2D) or line-far + 9 filter kernels (3D)
+    launches_per_hull = 5 + 2 * rounds + (9 if dim == 3 else 0)
 
     # ---------------- per-kernel pass (events after every launch)
     tr = P.trace(local)
