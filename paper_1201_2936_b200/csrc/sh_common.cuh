@@ -49,6 +49,7 @@ constexpr uint32_t ST_EMPTY = 2;
 constexpr uint32_t ST_DEGENERATE = 3;
 constexpr uint32_t ST_ROUND_GUARD = 4;
 constexpr uint32_t ST_SEG_OVERFLOW = 6;
+constexpr uint32_t ST_NONFINITE = 8;
 
 constexpr uint32_t FL_COLLINEAR = 1;
 
@@ -161,6 +162,8 @@ struct DevState {
   uint32_t arrive_book;   // K3 blocks that have read rp (reset by K3's finalizer)
   uint32_t ctr_red;       // last-block counter for reductions
   uint32_t book_small;    // K3 runs in one block (few children); set by K2
+  uint32_t nonfinite;     // K0 saw a NaN / inf coordinate
+  uint32_t pad1;
   // ---- traces (per round r, index r-1) ----
   uint32_t tr_live[MAX_TRACE];
   uint32_t tr_kept[MAX_TRACE];

@@ -413,6 +413,7 @@ static int fetch(sh_ctx* c, sh_result* res, cudaStream_t s) {
     }
   }
   if (h->status == ST_SEG_OVERFLOW || h->status == ST_CAND_OVERFLOW) return SH_OK;  // caller retries
+  if (h->status == ST_NONFINITE) return set_err(SH_CONTRACT, "coordinates must be finite");
   if (h->status == ST_DEGENERATE)
     return set_err(SH_DEGENERATE, "all points are coplanar; project to the plane and use the 2D driver");
   if (h->status == ST_ROUND_GUARD) return set_err(SH_ROUND_GUARD, "round count exceeded the input size");

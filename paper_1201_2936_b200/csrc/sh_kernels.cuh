@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
     st->ctr_book = 0;
     st->arrive_book = 0;
     st->book_small = 1;
+    st->nonfinite = 0;
     st->ctr_red = 0;
     st->dmax_bits = 0;
     st->rp.active = 0;
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   auto visit = [&](const LexRec& q) {
 #pragma unroll
     for (int k = 0; k < DIM; k++) {
+      if (!isfinite(q.c[k])) st->nonfinite = 1;  // geometry.py:38-40: coordinates must be finite
       r.lo[k] = fmin(r.lo[k], q.c[k]);
       r.hi[k] = fmax(r.hi[k], q.c[k]);
     }
@@ -255,6 +257,13 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   }
   const FirstRed t = s_w[0];
   st->ctr_red = 0;
+  __threadfence();
+  if (*(volatile uint32_t*)&st->nonfinite) {  // ContractViolation, nothing else runs
+    st->status = ST_NONFINITE;
+    st->h_final = 0;
+    st->first_active = 0;
+    return;
+  }
   // Tolerance.effective: eps_rel * np.hypot.reduce(spans)
   double acc = sub(t.hi[0], t.lo[0]);
 #pragma unroll

@@ -252,3 +252,19 @@ def test_scaled_and_shifted_inputs():
     x, y = generate("uniform-disk", 500_000, 4)
     for sc, sh in ((1e-150, 0.0), (1e150, 0.0), (1.0, 1e9), (3.0, -7.0)):
         _check2((x * sc + sh, y * sc + sh))
+
+
+def test_nonfinite_device_input_is_a_contract_violation():
+    """geometry.py:38-40 -- checked on the device inside the first pass."""
+    for bad in (np.nan, np.inf, -np.inf):
+        x, y = generate("uniform-disk", 100_000, 1)
+        x = x.copy()
+        x[77_777] = bad
+        with pytest.raises(P.ContractViolation):
+            P.hull_indices_2d(dev((x, y)))
+        cols = [c.copy() for c in generate("uniform-ball", 50_000, 1)]
+        cols[2][123] = bad
+        with pytest.raises(P.ContractViolation):
+            P.hull_indices_3d(dev(tuple(cols)))
+    # the context stays usable
+    _check2(generate("uniform-disk", 100_000, 1))
