@@ -13,14 +13,14 @@ from .errors import ContractViolation, DegenerateInputError, EmptyInputError
 from .geometry import PointSet, Tolerance
 from .primitives import (PermutationMap, ScanSpec, compact, flag_permute, head_index_broadcast,
                          reduce_broadcast, scatter, segment_ids, segmented_scan)
-from .quickhull import (HullResult, hull_indices_2d, hull_indices_3d, quickhull_2d, quickhull_3d,
-                        trace)
+from .quickhull import (HullResult, hull_indices_2d, hull_indices_3d, order_hull_2d, quickhull_2d,
+                        quickhull_3d, trace)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "ContractViolation", "DegenerateInputError", "EmptyInputError", "HullResult", "PermutationMap",
     "PointSet", "ScanSpec", "Tolerance", "compact", "flag_permute", "head_index_broadcast",
-    "hull_indices_2d", "hull_indices_3d", "quickhull_2d", "quickhull_3d", "reduce_broadcast",
+    "hull_indices_2d", "hull_indices_3d", "order_hull_2d", "quickhull_2d", "quickhull_3d", "reduce_broadcast",
     "scatter", "segment_ids", "segmented_scan", "trace",
 ]

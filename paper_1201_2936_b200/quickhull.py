@@ -197,6 +197,30 @@ def quickhull_2d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
     return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx)
 
 
+def order_hull_2d(vertices: PointSet) -> PointSet:
+    """CCW boundary order of a convex vertex set, starting at the
+    lexicographically smallest vertex (reference quickhull.py:449-461: angle
+    sort around the centroid, stable).  The angles and the sort run on the
+    GPU; the result equals the reference's order whenever no two vertices
+    share an angle from the centroid (always, for a strictly convex set)."""
+    if vertices.dim != 2:
+        raise ContractViolation("order_hull_2d needs 2D points")
+    if vertices.n < 3:
+        return vertices
+    x, y = (torch.from_numpy(c).to(torch.device("cuda", torch.cuda.current_device()))
+            for c in vertices.coords)
+    ang = torch.atan2(y - y.mean(), x - x.mean())
+    order = torch.sort(ang, stable=True).indices
+    xs, ys = x[order], y[order]
+    # lexicographic minimum over (x, y, position), lowest position among ties
+    xmin = xs.min()
+    cand = torch.nonzero(xs == xmin).flatten()
+    ymin = ys[cand].min()
+    start = int(cand[ys[cand] == ymin][0])
+    xs, ys = torch.roll(xs, -start), torch.roll(ys, -start)
+    return PointSet((xs.cpu().numpy(), ys.cpu().numpy()))
+
+
 def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
     """3D hull vertex set (reference quickhull.py:282-446), computed on the GPU."""
     _validate(points, 3)

@@ -268,3 +268,25 @@ def test_nonfinite_device_input_is_a_contract_violation():
             P.hull_indices_3d(dev(tuple(cols)))
     # the context stays usable
     _check2(generate("uniform-disk", 100_000, 1))
+
+
+def test_order_hull_2d_matches_reference_on_golden():
+    """order_hull_2d (quickhull.py:449-461) on the reference's own 2D hulls:
+    CCW from the lexicographic minimum, byte-identical."""
+    import json
+    import os
+    checked = 0
+    for case in C2:
+        if case.verts is None or case.verts.shape[0] < 3:
+            continue
+        v = P.PointSet((case.verts[:, 0].copy(), case.verts[:, 1].copy()))
+        got = P.order_hull_2d(v).as_rows()
+        # expected: convex polygon CCW from lex-min (restated exactly)
+        rows = case.verts
+        c = rows.mean(axis=0)
+        order = np.argsort(np.arctan2(rows[:, 1] - c[1], rows[:, 0] - c[0]), kind="stable")
+        r = rows[order]
+        start = min(range(len(r)), key=lambda i: (r[i, 0], r[i, 1], i))
+        assert got.tobytes() == np.roll(r, -start, axis=0).tobytes()
+        checked += 1
+    assert checked > 20
