@@ -70,7 +70,13 @@ int sh_hull2d(sh_ctx* ctx, const double* x, const double* y, int64_t stride, int
 /* 3D hull: vertex indices of the extreme points (reference result after
  * _extreme_vertex_mask, quickhull.py:136-164).  out_facets (optional, may
  * be NULL): int32 triples (i, j, k) of original indices, counter-clockwise
- * seen from outside, capacity facet_cap triples. */
+ * seen from outside (det[[p_i 1];[p_j 1];[p_k 1];[s 1]] > 0 for every other
+ * vertex s), capacity facet_cap triples (2*h - 4 suffice); res->facets = the
+ * number written.  The reference has no facet output; these are the facets
+ * of the hull of the returned vertices, exact (coplanar vertices are
+ * triangulated consistently by symbolic perturbation), in unspecified order.
+ * SH_CONTRACT if facet_cap is too small or the loop emitted >= 2^21
+ * candidate vertices. */
 int sh_hull3d(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride,
               int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* out_facets,
               int64_t facet_cap, sh_result* res, void* stream);
@@ -105,6 +111,13 @@ int sh_reserve(sh_ctx* ctx, int dim, int64_t n);
 /* Host-side self test of the glibc-hypot port used for eps and 2D edge
  * lengths (no GPU needed). */
 void sh_hypot_host(const double* x, const double* y, double* out, int64_t n);
+
+/* Host self test of the exact orientation predicates used by the 3D facet
+ * builder (no GPU needed): for each of nq queries, dim+1 points of `dim`
+ * doubles (pts) with their global indices (ids), out = sign of
+ * det [[p_i, 1]] under Simulation of Simplicity (never 0 for distinct ids).
+ * exact_only: skip the fp64 filter. */
+int sh_orient_host(int dim, const double* pts, const int64_t* ids, int64_t nq, int exact_only, int32_t* out);
 
 /* 0 (default): one CUDA-graph launch per hull, round loop on the device.
  * 1: host-driven round loop (one sync per round) -- for profilers that can

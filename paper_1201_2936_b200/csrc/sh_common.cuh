@@ -141,6 +141,8 @@ struct DevState {
   uint32_t use_eps_abs;
   uint32_t segcap;        // capacity of segment tables
   int64_t* out_idx;       // user output (device), capacity n
+  int32_t* out_facets;    // 3D facet triples (device), NULL = not requested
+  int64_t facet_cap;      // triples out_facets can hold
   // ---- first split (K0/K0b) ----
   double eps;
   uint32_t imin, imax, ifar;
@@ -204,6 +206,12 @@ struct Workspace {
 };
 
 // ---------------------------------------------------------------- helpers
+__device__ __forceinline__ unsigned long long pow2_dev(unsigned long long x) {
+  unsigned long long p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
 __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
   return *(const volatile uint64_t*)p;
 }

@@ -62,15 +62,14 @@ struct FilterParams {
 };
 
 struct FilterWs {
-  unsigned long long* result;  // [0] kept, [1] facets, [2] filter applied, [3] ambiguous
-  int32_t* out_facets;
-  int64_t facet_cap;
+  unsigned long long* result;  // [0] kept, [1] facets, [2] filter applied, [3] ambiguous, [4] facet status
   uint32_t mcap;
   FilterParams* fp;
   double *cx, *cy, *cz;              // candidates, discovery order
   uint32_t* ccell;
   double *sx, *sy, *sz;              // candidates sorted by cell
   uint32_t* sid;                     // discovery index of sorted entry
+  uint32_t* spos;                    // sorted position of discovery index
   uint32_t *cell_cnt, *cell_start, *cell_cur;
   double* nbox;                      // [node][6]: lo x,y,z, hi x,y,z (all levels)
   uint8_t* keep;
@@ -91,6 +90,7 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
   A((void**)&f.sz, mcap * 8);
   A((void**)&f.ccell, mcap * 4);
   A((void**)&f.sid, mcap * 4);
+  A((void**)&f.spos, mcap * 4);
   A((void**)&f.keep, mcap);
   A((void**)&f.cell_cnt, cells * 4);
   A((void**)&f.cell_start, (cells + 1) * 4);
@@ -101,22 +101,11 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
 }
 
 static inline void filter_free(FilterWs& f) {
-  void* ps[] = {f.result, f.fp, f.cx, f.cy, f.cz, f.sx, f.sy, f.sz, f.ccell, f.sid, f.keep,
+  void* ps[] = {f.result, f.fp, f.cx, f.cy, f.cz, f.sx, f.sy, f.sz, f.ccell, f.sid, f.spos, f.keep,
                 f.cell_cnt, f.cell_start, f.cell_cur, f.nbox};
   for (void* p : ps)
     if (p) cudaFree(p);
-  int32_t* of = f.out_facets;
-  int64_t fc = f.facet_cap;
   f = FilterWs{};
-  f.out_facets = of;
-  f.facet_cap = fc;
-}
-
-static inline int filter_set_params(FilterWs& f, int32_t* facets, int64_t cap, cudaStream_t s) {
-  (void)s;
-  f.out_facets = facets;
-  f.facet_cap = cap;
-  return 0;
 }
 
 // per-warp diagnostics (every lane holds the same values)
@@ -317,6 +306,7 @@ __global__ void __launch_bounds__(BLOCK) k_f_scatter(FilterWs f) {
     f.sy[p] = f.cy[i];
     f.sz[p] = f.cz[i];
     f.sid[p] = i;
+    f.spos[i] = p;
   }
 }
 
@@ -978,6 +968,7 @@ __global__ void __launch_bounds__(1024) k_f_compact(Workspace ws, FilterWs f) {
     f.result[1] = 0;
     f.result[2] = 1;
     f.result[3] = f.fp->ambiguous;
+    f.result[4] = 0;
   }
 }
 

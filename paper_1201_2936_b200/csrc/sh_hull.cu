@@ -20,6 +20,7 @@
 
 #include "../../include/seghull_b200.h"
 #include "sh_book.cuh"
+#include "sh_facets3.cuh"
 #include "sh_filter3.cuh"
 #include "sh_kernels.cuh"
 #include "sh_prims.cuh"
@@ -51,11 +52,14 @@ struct sh_ctx {
   unsigned long long* bbox_bits = nullptr;  // sh_bbox scratch
   Workspace ws{};
   FilterWs fws{};
+  FacetWs facws{};       // 3D facet output (allocated on the first facet request)
+  int fac_occ = 1;
   size_t red_bytes = 0;
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[4];
   int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0, round1_occ2 = 0, round1_occ3 = 0;
   uint32_t last_n = 0;
+  bool last_facets = false;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
   // per-launch CUDA events (launch_mode 2): ev0[i] / ev1[i] right before /
   // after launch i, whose kernel is prof_kind[i]
@@ -68,7 +72,7 @@ struct sh_ctx {
 
 // Kernel ids reported by sh_launch_times (include/seghull_b200.h).
 enum { KID_INIT = 0, KID_FIRST_REDUCE, KID_LINE_FAR, KID_ROUND_FIRST, KID_ROUND, KID_BOOK,
-       KID_FILTER, KID_OUTPUT };
+       KID_FILTER, KID_OUTPUT, KID_FACETS };
 
 // launch mode 2: bracket the next launch with events
 static void prof_begin(sh_ctx* c, cudaStream_t s) {
@@ -132,6 +136,7 @@ static void free_ws(sh_ctx* c) {
   cudaFree(w.red);
   cudaFree(w.st);
   filter_free(c->fws);
+  facet_free(c->facws);
   w = Workspace{};
   c->fws = FilterWs{};
   for (auto& g : c->g) {
@@ -266,12 +271,18 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
 }
 
 template <int DIM>
-static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
+static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s, bool facets) {
   if (DIM == 3) {
     prof_begin(c, s);
     int rc = filter_launch(c->fws, ws, c->nsm, s);
     if (rc) return set_err(rc, std::string("3D filter launch: ") + cudaGetErrorString(cudaGetLastError()));
     prof_mark(c, s, KID_FILTER);
+    if (facets) {
+      prof_begin(c, s);
+      rc = facet_launch(c->facws, c->fws, ws, c->nsm, c->fac_occ, s);
+      if (rc) return set_err(rc, std::string("3D facet launch: ") + cudaGetErrorString(cudaGetLastError()));
+      prof_mark(c, s, KID_FACETS);
+    }
     return SH_OK;
   }
   prof_begin(c, s);
@@ -281,9 +292,10 @@ static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s) {
   return SH_OK;
 }
 
+// graph slots: 2 = 2D, 3 = 3D vertices, 1 = 3D vertices + facets
 template <int DIM>
-static int build_graph(sh_ctx* c) {
-  Graph& G = c->g[DIM];
+static int build_graph(sh_ctx* c, bool facets = false) {
+  Graph& G = c->g[(DIM == 3 && facets) ? 1 : DIM];
   if (G.exec) return SH_OK;
   cudaStream_t s = c->build_stream;
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -314,7 +326,7 @@ static int build_graph(sh_ctx* c) {
   CK(cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CK(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
-  rc = launch_post<DIM>(c, ws, s);
+  rc = launch_post<DIM>(c, ws, s, facets);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(s, &graph);
   if (rc) return rc;
@@ -344,7 +356,21 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
   CK(cudaSetDevice(c->device));
   int rc = ensure_ws(c, DIM, (uint64_t)n, segcap_min, mcap_min);
   if (rc) return rc;
-  rc = build_graph<DIM>(c);
+  const bool want_facets = DIM == 3 && facets != nullptr;
+  if (want_facets && facet_cap < 0) return set_err(SH_CONTRACT, "facet_cap must be >= 0");
+  if (want_facets && c->facws.mcap < c->mcap) {
+    facet_free(c->facws);
+    Graph& g1 = c->g[1];
+    if (g1.exec) cudaGraphExecDestroy(g1.exec);
+    if (g1.graph) cudaGraphDestroy(g1.graph);
+    g1 = Graph{};
+    if (facet_alloc(c->facws, c->mcap)) {
+      facet_free(c->facws);
+      cudaGetLastError();
+      return set_err(SH_NOMEM, "device allocation failed for the facet workspace");
+    }
+  }
+  rc = build_graph<DIM>(c, want_facets);
   if (rc) return rc;
   // call parameters -> device (pinned mirror, one small async copy)
   DevState* h = c->st_host;
@@ -359,15 +385,12 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
   h->eps_abs = std::isnan(eps_abs) ? 0.0 : eps_abs;
   h->segcap = c->segcap;
   h->out_idx = out_idx;
-  c->fws.out_facets = facets;
-  c->fws.facet_cap = facet_cap;
+  h->out_facets = want_facets ? facets : nullptr;
+  h->facet_cap = want_facets ? facet_cap : 0;
   CK(cudaMemcpyAsync(c->ws.st, h, offsetof(DevState, eps), cudaMemcpyHostToDevice, s));
-  if (DIM == 3) {
-    int frc = filter_set_params(c->fws, facets, facet_cap, s);
-    if (frc) return frc;
-  }
+  c->last_facets = want_facets;
   if (c->launch_mode == 0) {
-    CK(cudaGraphLaunch(c->g[DIM].exec, s));
+    CK(cudaGraphLaunch(c->g[want_facets ? 1 : DIM].exec, s));
   } else {
     // host-driven loop: same kernels, one host sync per round (ncu can not
     // attribute kernels inside graphs that contain conditional nodes)
@@ -384,7 +407,7 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
       rc = launch_body<DIM>(c, ws, s);
       if (rc) return rc;
     }
-    rc = launch_post<DIM>(c, ws, s);
+    rc = launch_post<DIM>(c, ws, s, want_facets);
     c->prof_on = false;
     if (rc) return rc;
   }
@@ -394,7 +417,7 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
 
 static int fetch(sh_ctx* c, sh_result* res, cudaStream_t s) {
   CK(cudaMemcpyAsync(c->st_host, c->ws.st, offsetof(DevState, tr_live), cudaMemcpyDeviceToHost, s));
-  uint64_t fres[4] = {0, 0, 0, 0};
+  uint64_t fres[5] = {0, 0, 0, 0, 0};
   if (c->dim == 3) CK(cudaMemcpyAsync(fres, c->fws.result, sizeof(fres), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const DevState* h = c->st_host;
@@ -409,8 +432,14 @@ static int fetch(sh_ctx* c, sh_result* res, cudaStream_t s) {
     if (c->dim == 3) {
       res->h = (int64_t)fres[0];
       res->pruned = (int64_t)h->h_final - (int64_t)fres[0];
-      res->facets = (int64_t)fres[1];
+      res->facets = c->last_facets ? (int64_t)fres[1] : 0;
     }
+  }
+  if (c->dim == 3 && c->last_facets && h->status == ST_OK) {
+    if (fres[4] == ST_FAC_TOO_MANY)
+      return set_err(SH_CONTRACT, "facet output supports fewer than 2^21 candidate vertices");
+    if (fres[4] == ST_FAC_OVERFLOW)
+      return set_err(SH_CONTRACT, "facet_cap too small: " + std::to_string(fres[1]) + " facets");
   }
   if (h->status == ST_SEG_OVERFLOW || h->status == ST_CAND_OVERFLOW) return SH_OK;  // caller retries
   if (h->status == ST_NONFINITE) return set_err(SH_CONTRACT, "coordinates must be finite");
@@ -490,6 +519,9 @@ int sh_create(int device, sh_ctx** out) {
   c->round1_occ3 = std::max(1, o3b);
   int ob2 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
+  int of = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_fac_wrap, FAC_BLOCK, 0);
+  c->fac_occ = std::max(1, of);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob2, k_book<2>, BLOCK, 0);
   c->round_occ2 = std::max(1, o2);
   c->round_occ3 = std::max(1, o3);
@@ -589,6 +621,21 @@ int64_t sh_trace(sh_ctx* c, int64_t* live, int64_t* kept, int64_t* nseg, int64_t
 
 void sh_hypot_host(const double* x, const double* y, double* out, int64_t n) {
   for (int64_t i = 0; i < n; i++) out[i] = sh::glibc_hypot(x[i], y[i]);
+}
+
+int sh_orient_host(int dim, const double* pts, const int64_t* ids, int64_t nq, int exact_only, int32_t* out) {
+  if ((dim != 2 && dim != 3) || nq < 0 || !pts || !ids || !out) return set_err(SH_CONTRACT, "bad arguments");
+  const int R = dim + 1;
+  for (int64_t q = 0; q < nq; q++) {
+    const double* p = pts + q * R * dim;
+    const int64_t* I = ids + q * R;
+    if (dim == 2)
+      out[q] = exact_only ? sh::orient_sos<2>(p, I) : sh::orient2d_exact(p, p + 2, p + 4, I[0], I[1], I[2]);
+    else
+      out[q] = exact_only ? sh::orient_sos<3>(p, I)
+                          : sh::orient3d_exact(p, p + 3, p + 6, p + 9, I[0], I[1], I[2], I[3]);
+  }
+  return SH_OK;
 }
 
 int sh_set_launch_mode(sh_ctx* c, int mode) {

@@ -45,6 +45,7 @@ class HullResult:
     discarded: int
     warnings: list = field(default_factory=list)
     indices: np.ndarray = None
+    facets: np.ndarray = None  # 3D, quickhull_3d(..., facets=True): (f, 3) original indices
 
 
 def _raise_for(rc: int):
@@ -132,8 +133,10 @@ def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False):
 
 def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False):
     """Original indices (int64 tensor) of the 3D hull vertices, plus the
-    (f, 3) int32 facet triples when ``facets`` is true.  Host input is
-    handled like in hull_indices_2d."""
+    (f, 3) int32 facet triples when ``facets`` is true: original indices,
+    counter-clockwise seen from outside, exact (coplanar vertices are
+    triangulated consistently), order unspecified.  Host input is handled
+    like in hull_indices_2d."""
     if _on_host(points):
         r = hull_indices_3d(_to_cuda(points), tol, facets, return_info)
         if return_info:
@@ -144,14 +147,21 @@ def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_i
     if n == 0:
         raise EmptyInputError("cannot take the hull of an empty point set")
     out = torch.empty(n, dtype=torch.int64, device=keep[0].device)
-    fcap = 2 * n + 8 if facets else 0
-    fout = torch.empty((max(fcap, 1), 3), dtype=torch.int32, device=keep[0].device)
-    res = _lib.ShResult()
-    with torch.cuda.device(device):
-        rc = _lib.lib().sh_hull3d(_lib.context(device), ptrs[0], ptrs[1], ptrs[2], stride, n,
-                                  tol.eps_rel, tol.eps_abs, out.data_ptr(),
-                                  fout.data_ptr() if facets else None, fcap, ctypes.byref(res),
-                                  _stream_ptr(device))
+    # facets <= 2 * vertices - 4; start from a size that covers volume-like
+    # clouds and retry once with the exact count for surface-like ones
+    fcap = min(2 * n + 8, max(4096, 16 * int(n ** 0.5))) if facets else 0
+    for _ in range(2):
+        fout = torch.empty((max(fcap, 1), 3), dtype=torch.int32, device=keep[0].device)
+        res = _lib.ShResult()
+        with torch.cuda.device(device):
+            rc = _lib.lib().sh_hull3d(_lib.context(device), ptrs[0], ptrs[1], ptrs[2], stride, n,
+                                      tol.eps_rel, tol.eps_abs, out.data_ptr(),
+                                      fout.data_ptr() if facets else None, fcap, ctypes.byref(res),
+                                      _stream_ptr(device))
+        if facets and rc == _lib.SH_CONTRACT and res.facets > fcap:
+            fcap = int(res.facets)
+            continue
+        break
     if rc != _lib.SH_OK:
         _raise_for(rc)
     idx = out[:res.h]
@@ -221,11 +231,13 @@ def order_hull_2d(vertices: PointSet) -> PointSet:
     return PointSet((xs.cpu().numpy(), ys.cpu().numpy()))
 
 
-def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
-    """3D hull vertex set (reference quickhull.py:282-446), computed on the GPU."""
+def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance(), facets: bool = False) -> HullResult:
+    """3D hull vertex set (reference quickhull.py:282-446), computed on the
+    GPU.  ``facets=True`` (not in the reference) also fills
+    ``HullResult.facets`` with the hull's triangles."""
     _validate(points, 3)
     cols = _to_device(points)
-    idx, _, res = hull_indices_3d(cols, tol, return_info=True)
+    idx, fac, res = hull_indices_3d(cols, tol, facets=facets, return_info=True)
     idx = idx.cpu().numpy()
     warnings = []
     if res.flags & _lib.SH_FLAG_COLLINEAR:
@@ -238,4 +250,5 @@ def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
         warnings.append(f"pruned {int(res.pruned)} non-extreme candidate vertex(es) emitted by "
                         "incomplete per-face outside sets")  # :308-310
     verts = PointSet(tuple(c[idx] for c in points.coords)) if idx.size else PointSet.empty(3)
-    return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx)
+    return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx,
+                      fac.cpu().numpy() if fac is not None else None)
