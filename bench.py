@@ -260,6 +260,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--facets", action="store_true",
+                    help="3D configs: also build the facet triples inside every step")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (sharded) pipeline even at N=1")
     args = ap.parse_args()
@@ -302,7 +304,10 @@ def main():
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     out = torch.empty(n, dtype=torch.int64, device="cuda")
-    fac = None
+    want_fac = args.facets and dim == 3
+    fcap = 4 * n + 8 if want_fac else 0  # n is at most 2^28 here; cap covers 2*candidates
+    fac = torch.empty((max(min(fcap, 1 << 24), 1), 3), dtype=torch.int32, device="cuda")
+    fcap = min(fcap, 1 << 24)
     res = _lib.ShResult()
     ptrs = [t.data_ptr() for t in d]
     nan = float("nan")
@@ -312,12 +317,17 @@ def main():
             rc = L.sh_hull2d_async(ctx, ptrs[0], ptrs[1], 1, n, 1e-12, nan, out.data_ptr(), sp)
         else:
             rc = L.sh_hull3d_async(ctx, ptrs[0], ptrs[1], ptrs[2], 1, n, 1e-12, nan, out.data_ptr(),
-                                   None, 0, sp)
+                                   fac.data_ptr() if want_fac else None, fcap, sp)
         if rc:
             raise RuntimeError(_lib.last_error())
 
     # sync API once: sizes the segment tables (overflow retries happen here)
-    f = P.hull_indices_2d if dim == 2 else P.hull_indices_3d
+    if dim == 2:
+        f = P.hull_indices_2d
+    else:
+        def f(pts):
+            r = P.hull_indices_3d(pts, facets=want_fac)
+            return r[0] if want_fac else r
     f(d)
     for _ in range(args.warmup):
         launch()
@@ -349,7 +359,7 @@ def main():
     value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
     # init, first reduce, first-split count, book, then (round, book) per
     # round, then output (2D) or line-far + 9 filter kernels (3D)
-    launches_per_hull = 5 + 2 * rounds + (9 if dim == 3 else 0)
+    launches_per_hull = 5 + 2 * rounds + (9 if dim == 3 else 0) + (4 if want_fac else 0)
 
     # ---------------- per-kernel pass (events after every launch)
     tr = P.trace(local)
@@ -383,7 +393,7 @@ def main():
         if best is None or tot_round < best[0]:
             best = (tot_round, float(ms.sum()), rt)
             names = ["init", "first_reduce", "line_far", "round_first", "round", "book", "filter",
-                     "output"]
+                     "output", "facets"]
             kernel_ms_by_kind = {names[k]: round(float(ms[kinds == k].sum()), 4)
                                  for k in sorted(set(kinds.tolist()))}
     peak, peak_src = measured_peak()
@@ -438,8 +448,10 @@ def main():
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc, "n": n, "dim": dim, "rounds": rounds, "hull": h,
+                "config": {"workload": desc + (" + facet triples" if want_fac else ""), "n": n,
+                           "dim": dim, "rounds": rounds, "hull": h,
                            "candidates": int(res.candidates), "eps_rel": 1e-12,
+                           "facets": int(res.facets) if want_fac else None,
                            "l2": "inputs (%.1f GB) larger than the 126 MB L2; no flush" %
                                  (8 * dim * n / 1e9),
                            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},

@@ -138,6 +138,13 @@ int64_t sh_launch_times(sh_ctx* ctx, int32_t* kind, float* ms, int64_t cap);
  * resolved by the global GJK.  Returns the count written (<= cap, <= 11). */
 int sh_filter_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
 
+/* Diagnostics of the last 3D facet build: facets, queue items, wrap
+ * queries, 32-point batches scanned, batches with a better candidate, box
+ * tree nodes visited, SM cycles in wrap queries / waiting on the queue
+ * (summed over warps), cycles of the initial-facet search.  Returns the
+ * count written (<= cap, <= 9). */
+int sh_facet_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
+
 /* ---- framework primitives (device arrays) ----
  * Replace segments.segmented_scan (segments.py:201-234), flag_permute
  * (primitives.py:91-117), compact (:120-148) and scatter (:151-176).

@@ -55,10 +55,16 @@ struct FacetCtl {
   unsigned int head, reserved, completed, nfacets;
   unsigned int status, a0, b0, pad;
   unsigned long long fmask, emask, icap;
+  // diagnostics (sh_facet_stats)
+  unsigned long long queries, batches, beat_batches, nodes, wrap_cycles, wait_cycles, init_cycles;
 };
 
 struct FacetWs {
-  unsigned long long* ftab;   // facet keys (canonical rotation of discovery ids)
+  double *kx, *ky, *kz;       // kept vertices in Morton order (vertex id = position)
+  uint32_t* korig;            // their original point indices
+  double* knbox;              // box tree over them (layout of FilterWs::nbox)
+  FilterParams* kfp;          // its parameters (m = number of kept vertices)
+  unsigned long long* ftab;   // facet keys (canonical rotation of vertex ids)
   unsigned long long* etab;   // directed edge keys
   unsigned long long* items;  // work queue: (1 << 63) | a << 21 | b, 0 = not yet written
   FacetCtl* ctl;
@@ -81,12 +87,18 @@ static inline int facet_alloc(FacetWs& w, uint32_t mcap) {
   ok &= cudaMalloc((void**)&w.etab, w.ecap * 8) == cudaSuccess;
   ok &= cudaMalloc((void**)&w.items, w.icap * 8) == cudaSuccess;
   ok &= cudaMalloc((void**)&w.ctl, sizeof(FacetCtl)) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.kx, (size_t)mcap * 8 + 64) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.ky, (size_t)mcap * 8 + 64) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.kz, (size_t)mcap * 8 + 64) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.korig, (size_t)mcap * 4 + 64) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.knbox, ((size_t)mcap / 31 + 2 * F_LEVELS + 8) * 48) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.kfp, sizeof(FilterParams)) == cudaSuccess;
   w.mcap = mcap;
   return ok ? 0 : 1;
 }
 
 static inline void facet_free(FacetWs& w) {
-  void* ps[] = {w.ftab, w.etab, w.items, w.ctl};
+  void* ps[] = {w.ftab, w.etab, w.items, w.ctl, w.kx, w.ky, w.kz, w.korig, w.knbox, w.kfp};
   for (void* p : ps)
     if (p) cudaFree(p);
   w = FacetWs{};
@@ -155,6 +167,8 @@ __global__ void __launch_bounds__(BLOCK) k_fac_clear(Workspace ws, FilterWs f, F
     c->head = c->reserved = c->completed = c->nfacets = 0;
     c->status = (m >= (1u << FAC_ID_BITS)) ? ST_FAC_TOO_MANY : 0u;
     c->a0 = c->b0 = FAC_NONE;
+    c->queries = c->batches = c->beat_batches = c->nodes = 0;
+    c->wrap_cycles = c->wait_cycles = c->init_cycles = 0;
     c->fmask = fm - 1;
     c->emask = em - 1;
     c->icap = ic;
@@ -172,6 +186,7 @@ struct Wrap {
   double q[3];
   double n[3];        // (b - q) x (a - q)
   double P[3];        // |products| of n's components (error bound)
+  uint32_t nb, nbb, nn;  // diagnostics: batches, batches with a beating lane, tree nodes
 };
 
 __device__ __forceinline__ void wrap_set_q(Wrap& W, uint32_t iq, int64_t gq, const double* q) {
@@ -213,34 +228,45 @@ __device__ __forceinline__ bool wrap_beats_pair(const Wrap& W, const double* x, 
   return orient3d_exact(W.b, W.a, x, y, W.gb, W.ga, gx, gy) < 0;
 }
 
-struct FacTree {
-  const double *sx, *sy, *sz;
-  const uint32_t* sid;
-  const uint8_t* keep;
-  const uint32_t* vout;
+// The kept vertices in Morton order (a subsequence of the filter's sorted
+// candidates) with their own box tree: vertex ids in the facet builder are
+// positions in this order.
+struct KTree {
+  const double *x, *y, *z;
+  const uint32_t* orig;  // original point index (output, perturbation order)
+  const double* nbox;
 };
 
-// One 32-point batch (sorted positions p0 + lane): lanes whose point beats
+// One 32-vertex batch (positions p = base + lane): lanes whose vertex beats
 // q compete in a tournament, the winner becomes the new q.
-__device__ __forceinline__ void wrap_batch(Wrap& W, const FacTree& T, uint32_t m, uint32_t p) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void wrap_batch(Wrap& W, const KTree& T, uint32_t K, uint32_t p) {
   bool cand = false;
   double s[3] = {0.0, 0.0, 0.0};
   uint32_t id = FAC_NONE;
   int64_t gs = -1;
-  if (p < m) {
-    id = __ldg(&T.sid[p]);
-    if (__ldg(&T.keep[id]) && id != W.ia && id != W.ib && id != W.iq) {
-      s[0] = __ldg(&T.sx[p]);
-      s[1] = __ldg(&T.sy[p]);
-      s[2] = __ldg(&T.sz[p]);
-      gs = (int64_t)__ldg(&T.vout[id]);
-      cand = wrap_beats(W, s, gs);
-    }
+  if (p < K && p != W.ia && p != W.ib && p != W.iq) {
+    id = p;
+    s[0] = __ldg(&T.x[p]);
+    s[1] = __ldg(&T.y[p]);
+    s[2] = __ldg(&T.z[p]);
+    gs = (int64_t)__ldg(&T.orig[p]);
+    cand = wrap_beats(W, s, gs);
   }
   const uint32_t mask = __ballot_sync(0xFFFFFFFFu, cand);
+  W.nb++;
   if (!mask) return;
+  W.nbb++;
   if (!cand) id = FAC_NONE;
+  if (__popc(mask) == 1) {
+    const int src = __ffs(mask) - 1;
+    id = __shfl_sync(0xFFFFFFFFu, id, src);
+    gs = __shfl_sync(0xFFFFFFFFu, gs, src);
+    s[0] = __shfl_sync(0xFFFFFFFFu, s[0], src);
+    s[1] = __shfl_sync(0xFFFFFFFFu, s[1], src);
+    s[2] = __shfl_sync(0xFFFFFFFFu, s[2], src);
+    wrap_set_q(W, id, gs, s);
+    return;
+  }
   // butterfly tournament (strict total order => every lane ends with the max)
 #pragma unroll 1
   for (int o = 1; o < 32; o <<= 1) {
@@ -268,7 +294,7 @@ __device__ __forceinline__ bool wrap_box_may_beat(const Wrap& W, const double* b
   double bound = 0.0, perm = 0.0;
 #pragma unroll
   for (int k = 0; k < 3; k++) {
-    const double lo = sub(__ldg(bx + k), W.q[k]), hi = sub(__ldg(bx + 3 + k), W.q[k]);
+    const double lo = sub(bx[k], W.q[k]), hi = sub(bx[3 + k], W.q[k]);
     const double t = fmax(mul(lo, W.n[k]), mul(hi, W.n[k]));
     bound = (k == 0) ? t : add(bound, t);
     perm = add(perm, mul(fmax(fabs(lo), fabs(hi)), W.P[k]));
@@ -276,37 +302,58 @@ __device__ __forceinline__ bool wrap_box_may_beat(const Wrap& W, const double* b
   return !(bound < -mul(2.0 * WRAP_ERR, perm));
 }
 
+__device__ __forceinline__ void load_box(const double* src, double* bx) {
+#pragma unroll
+  for (int k = 0; k < 6; k++) bx[k] = __ldg(src + k);
+}
+
 // p of the facet (b, a, p) across the hull edge (a, b); every lane returns it
-__device__ uint32_t wrap_query(Wrap& W, const FacTree& T, const FilterParams& P, const FilterWs& f,
-                               uint32_t* stk) {
+__device__ uint32_t wrap_query(Wrap& W, const KTree& T, const FilterParams& P, uint32_t* stk) {
   const int lane = threadIdx.x & 31;
-  const uint32_t m = P.m;
-  // (1) the sorted neighbourhoods of a and b
-  const uint32_t pa = __ldg(&f.spos[W.ia]), pb = __ldg(&f.spos[W.ib]);
+  const uint32_t K = P.m;
+  // (1) the Morton neighbourhoods of a and b
 #pragma unroll 1
   for (int k = 0; k < 4; k++) {
-    const uint32_t c = (k < 2) ? pa : pb;
+    const uint32_t c = (k < 2) ? W.ia : W.ib;
     const uint32_t lo = c >= 32 ? c - 32 : 0;
-    wrap_batch(W, T, m, lo + (k & 1) * 32 + lane);
+    wrap_batch(W, T, K, lo + (k & 1) * 32 + lane);
   }
-  // (2) box-tree descent
+  // (2) box-tree descent (depth first); passing leaf children are scanned
+  // right away, each re-tested against the then current q
   if (P.nlev == 0) return W.iq;
-  int top = 0;
+  if (P.nlev == 1) {
+    wrap_batch(W, T, K, lane);
+    return W.iq;
+  }
+  int top = 1;
   stk[0] = ((P.nlev - 1) << 26) | 0u;
-  top = 1;
   while (top > 0) {
     top--;
     const uint32_t e = stk[top];
     __syncwarp();
     const uint32_t cl = e >> 26, cn = e & ((1u << 26) - 1);
-    if (!wrap_box_may_beat(W, f.nbox + (size_t)(P.loff[cl] + cn) * 6)) continue;
-    if (cl == 0) {
-      wrap_batch(W, T, m, cn * 32 + lane);
+    W.nn++;
+    double bx[6];
+    load_box(T.nbox + (size_t)(P.loff[cl] + cn) * 6, bx);
+    if (!wrap_box_may_beat(W, bx)) continue;
+    const uint32_t chl = cl - 1, ch = cn * 32 + lane;
+    bool pass = false;
+    if (ch < P.lnodes[chl]) {
+      load_box(T.nbox + (size_t)(P.loff[chl] + ch) * 6, bx);
+      pass = wrap_box_may_beat(W, bx);
+    }
+    uint32_t mask = __ballot_sync(0xFFFFFFFFu, pass);
+    if (chl == 0) {
+      bool first = true;
+      while (mask) {
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        if (!first && !__shfl_sync(0xFFFFFFFFu, wrap_box_may_beat(W, bx), l)) continue;
+        first = false;
+        wrap_batch(W, T, K, (cn * 32 + l) * 32 + lane);
+      }
       continue;
     }
-    const uint32_t chl = cl - 1, ch = cn * 32 + lane;
-    const bool pass = ch < P.lnodes[chl] && wrap_box_may_beat(W, f.nbox + (size_t)(P.loff[chl] + ch) * 6);
-    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, pass);
     const uint32_t r = __popc(mask & lanemask_lt());
     if (pass && top + (int)r < F_STACK) stk[top + r] = (chl << 26) | ch;
     top = min(top + __popc(mask), F_STACK);
@@ -315,38 +362,36 @@ __device__ uint32_t wrap_query(Wrap& W, const FacTree& T, const FilterParams& P,
   return W.iq;
 }
 
-__device__ __forceinline__ void load_pt(const FilterWs& f, uint32_t i, double* p) {
-  p[0] = f.cx[i];
-  p[1] = f.cy[i];
-  p[2] = f.cz[i];
-}
-
-__device__ __forceinline__ void wrap_begin(Wrap& W, const FilterWs& f, const uint32_t* vout, uint32_t a,
-                                           uint32_t b) {
+__device__ __forceinline__ void wrap_begin(Wrap& W, const KTree& T, uint32_t a, uint32_t b) {
   W.ia = a;
   W.ib = b;
-  load_pt(f, a, W.a);
-  load_pt(f, b, W.b);
-  W.ga = (int64_t)vout[a];
-  W.gb = (int64_t)vout[b];
+  W.a[0] = T.x[a];
+  W.a[1] = T.y[a];
+  W.a[2] = T.z[a];
+  W.b[0] = T.x[b];
+  W.b[1] = T.y[b];
+  W.b[2] = T.z[b];
+  W.ga = (int64_t)T.orig[a];
+  W.gb = (int64_t)T.orig[b];
   W.iq = FAC_NONE;
   W.gq = -1;
+  W.nb = W.nbb = W.nn = 0;
 }
 
-// Record the facet (x, y, z) (discovery ids) if new: output triple of
-// original indices, its directed edges into the edge set, and the open
-// edges (those whose twin is not known) onto the queue.  Warp-uniform
-// arguments; lane 0 does the work.  skip: edge index (0..2) not to push.
-__device__ void fac_emit(const FacetWs& w, const uint32_t* vout, int32_t* out, int64_t cap, uint32_t x,
+// Record the facet (x, y, z) (vertex ids) if new: output triple of original
+// indices, its directed edges into the edge set, and the open edges (those
+// whose twin is not known) onto the queue.  Warp-uniform arguments; lane 0
+// does the work.  skip: edge index (0..2) not to push.
+__device__ void fac_emit(const FacetWs& w, const uint32_t* orig, int32_t* out, int64_t cap, uint32_t x,
                          uint32_t y, uint32_t z, int skip) {
   if ((threadIdx.x & 31) != 0) return;
   FacetCtl* C = w.ctl;
   if (!hset_insert(w.ftab, C->fmask, facet_key(x, y, z))) return;
   const unsigned int pos = atomicAdd(&C->nfacets, 1u);
   if ((int64_t)pos < cap) {
-    out[3 * (size_t)pos + 0] = (int32_t)vout[x];
-    out[3 * (size_t)pos + 1] = (int32_t)vout[y];
-    out[3 * (size_t)pos + 2] = (int32_t)vout[z];
+    out[3 * (size_t)pos + 0] = (int32_t)orig[x];
+    out[3 * (size_t)pos + 1] = (int32_t)orig[y];
+    out[3 * (size_t)pos + 2] = (int32_t)orig[z];
   }
   const uint32_t u[3] = {x, y, z}, v[3] = {y, z, x};
   for (int k = 0; k < 3; k++) hset_insert(w.etab, C->emask, edge_key(u[k], v[k]));
@@ -364,139 +409,233 @@ __device__ void fac_emit(const FacetWs& w, const uint32_t* vout, int32_t* out, i
   }
 }
 
+// ------------------------------------------------------------------ F7a'
+// kept vertices (filter keep mask) in Morton order -> the facet builder's
+// vertex arrays, plus the parameters of their box tree
+__global__ void __launch_bounds__(1024) k_fac_keep(Workspace ws, FilterWs f, FacetWs w) {
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  const uint32_t m = f.fp->m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (!ws.st->out_facets) return;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < m; base += 1024) {
+    const uint32_t p = base + threadIdx.x;
+    uint32_t id = 0, v = 0;
+    if (p < m) {
+      id = f.sid[p];
+      v = f.keep[id] ? 1u : 0u;
+    }
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = s_w[lane];
+      uint32_t y = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
+        if (lane >= o) y += z;
+      }
+      s_w[lane] = y - x;
+    }
+    __syncthreads();
+    const uint32_t pos = s_carry + s_w[warp] + __popc(bal & lanemask_lt());
+    if (v) {
+      w.kx[pos] = f.sx[p];
+      w.ky[pos] = f.sy[p];
+      w.kz[pos] = f.sz[p];
+      w.korig[pos] = ws.vout[id];
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = pos + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    FilterParams* P = w.kfp;
+    const uint32_t K = s_carry;
+    P->m = K;
+    uint32_t nl = K ? (K + 31) / 32 : 0, off = 0, lev = 0;
+    for (int l = 0; l < F_LEVELS; l++) {
+      P->lnodes[l] = nl;
+      P->loff[l] = off;
+      if (nl) lev = l + 1;
+      off += nl;
+      nl = (nl <= 1) ? 0 : (nl + 31) / 32;
+    }
+    P->nlev = lev;
+  }
+}
+
 // ------------------------------------------------------------------ F7b
-__global__ void __launch_bounds__(1024) k_fac_init(Workspace ws, FilterWs f, FacetWs w) {
+// Seeds: the vertices of minimal / maximal perturbed x and y (xy
+// projection, virtual vertical line) and z (xz projection, virtual line
+// along y).  Perturbed minimum: smallest value, ties -> largest original
+// index (its perturbation is the smallest); maximum: ties -> smallest.
+constexpr int FAC_SEEDS = 6;
+
+__device__ __forceinline__ bool seed_better(int s, double v, int64_t g, double bv, int64_t bg) {
+  if (s & 1) return v > bv || (v == bv && g < bg);  // maximum
+  return v < bv || (v == bv && g > bg);             // minimum
+}
+
+__global__ void __launch_bounds__(1024) k_fac_init(Workspace ws, FacetWs w) {
+  const long long t_start = clock64();
   __shared__ FilterParams sP;
-  __shared__ uint32_t s_id[32];
-  __shared__ uint32_t s_stk[F_STACK];
-  __shared__ uint32_t s_a0;
-  if (threadIdx.x == 0) sP = *f.fp;
+  __shared__ uint32_t s_best[FAC_SEEDS][32];
+  __shared__ uint32_t s_a[FAC_SEEDS], s_b[FAC_SEEDS];
+  __shared__ uint32_t s_stk[FAC_SEEDS][F_STACK];
+  if (threadIdx.x == 0) sP = *w.kfp;
   __syncthreads();
   const FilterParams& P = sP;
-  const uint32_t m = P.m;
+  const uint32_t K = P.m;
   FacetCtl* C = w.ctl;
-  const uint32_t* vout = ws.vout;
   int32_t* out = ws.st->out_facets;
-  if (!out || m < 4 || C->status) return;
+  if (!out || K < 4 || C->status) return;
+  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // a0: minimal perturbed x = minimal x, ties -> highest original index
-  uint32_t best = FAC_NONE;
-  double bx = 0.0;
-  int64_t bg = -1;
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    if (!f.keep[i]) continue;
-    const double x = f.cx[i];
-    const int64_t g = vout[i];
-    if (best == FAC_NONE || x < bx || (x == bx && g > bg)) {
-      best = i;
-      bx = x;
-      bg = g;
+  // (A) the six perturbed axis extremes
+  {
+    uint32_t best[FAC_SEEDS];
+    double bv[FAC_SEEDS];
+    int64_t bg[FAC_SEEDS];
+    for (int s = 0; s < FAC_SEEDS; s++) {
+      best[s] = FAC_NONE;
+      bv[s] = 0.0;
+      bg[s] = -1;
     }
-  }
-  for (int o = 16; o; o >>= 1) {
-    const uint32_t ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-    const double ox = __shfl_xor_sync(0xFFFFFFFFu, bx, o);
-    const int64_t og = __shfl_xor_sync(0xFFFFFFFFu, bg, o);
-    if (ob != FAC_NONE && (best == FAC_NONE || ox < bx || (ox == bx && og > bg))) {
-      best = ob;
-      bx = ox;
-      bg = og;
+    for (uint32_t i = threadIdx.x; i < K; i += blockDim.x) {
+      const double c[3] = {T.x[i], T.y[i], T.z[i]};
+      const int64_t g = T.orig[i];
+      for (int s = 0; s < FAC_SEEDS; s++)
+        if (best[s] == FAC_NONE || seed_better(s, c[s >> 1], g, bv[s], bg[s])) {
+          best[s] = i;
+          bv[s] = c[s >> 1];
+          bg[s] = g;
+        }
     }
-  }
-  if (lane == 0) s_id[warp] = best;
-  __syncthreads();
-  if (warp == 0) {
-    best = s_id[lane];
-    bx = best != FAC_NONE ? f.cx[best] : 0.0;
-    bg = best != FAC_NONE ? (int64_t)vout[best] : -1;
-    for (int o = 16; o; o >>= 1) {
-      const uint32_t ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-      const double ox = __shfl_xor_sync(0xFFFFFFFFu, bx, o);
-      const int64_t og = __shfl_xor_sync(0xFFFFFFFFu, bg, o);
-      if (ob != FAC_NONE && (best == FAC_NONE || ox < bx || (ox == bx && og > bg))) {
-        best = ob;
-        bx = ox;
-        bg = og;
+    for (int s = 0; s < FAC_SEEDS; s++) {
+      for (int o = 16; o; o >>= 1) {
+        const uint32_t ob = __shfl_xor_sync(0xFFFFFFFFu, best[s], o);
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv[s], o);
+        const int64_t og = __shfl_xor_sync(0xFFFFFFFFu, bg[s], o);
+        if (ob != FAC_NONE && (best[s] == FAC_NONE || seed_better(s, ov, og, bv[s], bg[s]))) {
+          best[s] = ob;
+          bv[s] = ov;
+          bg[s] = og;
+        }
       }
+      if (lane == 0) s_best[s][warp] = best[s];
     }
-    if (lane == 0) s_a0 = best;
-  }
-  __syncthreads();
-  const uint32_t a0 = s_a0;
-  if (a0 == FAC_NONE) return;
-  const double A[2] = {f.cx[a0], f.cy[a0]};
-  const int64_t ga = vout[a0];
-  // b0: s beats q <=> orient2d(a0, q, s) < 0 (xy projection, same perturbation)
-  uint32_t q = FAC_NONE;
-  double Q[2] = {0.0, 0.0};
-  int64_t gq = -1;
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    if (!f.keep[i] || i == a0) continue;
-    const double S[2] = {f.cx[i], f.cy[i]};
-    const int64_t gs = vout[i];
-    if (q == FAC_NONE || orient2d_exact(A, Q, S, ga, gq, gs) < 0) {
-      q = i;
-      Q[0] = S[0];
-      Q[1] = S[1];
-      gq = gs;
+    __syncthreads();
+    if (warp < FAC_SEEDS) {
+      const int s = warp;
+      uint32_t b = s_best[s][lane];
+      double v = b != FAC_NONE ? (s < 2 ? T.x[b] : s < 4 ? T.y[b] : T.z[b]) : 0.0;
+      int64_t g = b != FAC_NONE ? (int64_t)T.orig[b] : -1;
+      for (int o = 16; o; o >>= 1) {
+        const uint32_t ob = __shfl_xor_sync(0xFFFFFFFFu, b, o);
+        const double ov = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        const int64_t og = __shfl_xor_sync(0xFFFFFFFFu, g, o);
+        if (ob != FAC_NONE && (b == FAC_NONE || seed_better(s, ov, og, v, g))) {
+          b = ob;
+          v = ov;
+          g = og;
+        }
+      }
+      if (lane == 0) s_a[s] = b;
     }
+    __syncthreads();
   }
-  auto tourney = [&]() {
+  // (B) per seed (5 warps each): the neighbour b on the projected 2D hull,
+  // s beats q <=> orient2d(a, q, s) < 0
+  const int sd = warp < 5 * FAC_SEEDS ? warp / 5 : 0;
+  const bool xz = sd >= 4;
+  const uint32_t a2 = s_a[sd];
+  const double A[2] = {T.x[a2], xz ? T.z[a2] : T.y[a2]};
+  const int64_t ga = T.orig[a2];
+  auto tourney = [&](uint32_t& q, double* Q, int64_t& gq) {
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t oq = __shfl_xor_sync(0xFFFFFFFFu, q, o);
-      const double ox = __shfl_xor_sync(0xFFFFFFFFu, Q[0], o), oy = __shfl_xor_sync(0xFFFFFFFFu, Q[1], o);
+      const double O[2] = {__shfl_xor_sync(0xFFFFFFFFu, Q[0], o), __shfl_xor_sync(0xFFFFFFFFu, Q[1], o)};
       const int64_t og = __shfl_xor_sync(0xFFFFFFFFu, gq, o);
-      const double O[2] = {ox, oy};
       if (oq != FAC_NONE && (q == FAC_NONE || orient2d_exact(A, Q, O, ga, gq, og) < 0)) {
         q = oq;
-        Q[0] = ox;
-        Q[1] = oy;
+        Q[0] = O[0];
+        Q[1] = O[1];
         gq = og;
       }
     }
   };
-  tourney();
-  if (lane == 0) s_id[warp] = q;
-  __syncthreads();
-  if (warp != 0) return;
-  q = s_id[lane];
-  Q[0] = q != FAC_NONE ? f.cx[q] : 0.0;
-  Q[1] = q != FAC_NONE ? f.cy[q] : 0.0;
-  gq = q != FAC_NONE ? (int64_t)vout[q] : -1;
-  tourney();
-  const uint32_t b0 = q;
-  if (b0 == FAC_NONE) return;
-  // first facet: wrap (a0, b0) against the vertical half-plane through a0
-  FacTree T{f.sx, f.sy, f.sz, f.sid, f.keep, vout};
-  Wrap W;
-  wrap_begin(W, f, vout, a0, b0);
-  const uint32_t p = wrap_query(W, T, P, f, s_stk);
-  if (lane == 0) {
-    C->a0 = a0;
-    C->b0 = b0;
+  if (warp < 5 * FAC_SEEDS) {
+    const uint32_t gt = threadIdx.x - sd * 160;
+    uint32_t q = FAC_NONE;
+    double Q[2] = {0.0, 0.0};
+    int64_t gq = -1;
+    for (uint32_t i = gt; i < K; i += 160) {
+      if (i == a2) continue;
+      const double S[2] = {T.x[i], xz ? T.z[i] : T.y[i]};
+      const int64_t gs = T.orig[i];
+      if (q == FAC_NONE || orient2d_exact(A, Q, S, ga, gq, gs) < 0) {
+        q = i;
+        Q[0] = S[0];
+        Q[1] = S[1];
+        gq = gs;
+      }
+    }
+    tourney(q, Q, gq);
+    if (lane == 0) s_best[sd][warp - 5 * sd] = q;
   }
-  if (p == FAC_NONE) return;
-  fac_emit(w, vout, out, ws.st->facet_cap, b0, a0, p, -1);
+  __syncthreads();
+  if (warp < 5 * FAC_SEEDS && warp == 5 * sd) {
+    uint32_t q = lane < 5 ? s_best[sd][lane] : FAC_NONE;
+    double Q[2] = {q != FAC_NONE ? T.x[q] : 0.0, q != FAC_NONE ? (xz ? T.z[q] : T.y[q]) : 0.0};
+    int64_t gq = q != FAC_NONE ? (int64_t)T.orig[q] : -1;
+    tourney(q, Q, gq);
+    if (lane == 0) s_b[sd] = q;
+  }
+  __syncthreads();
+  // (C) one warp per seed: the hull facet across the silhouette edge.  In
+  // the xy projection the virtual facet is (a, b, a + e_z), so wrap(a, b)
+  // gives the facet (b, a, p); in the xz projection it is (b, a, a + e_y)
+  // and wrap(b, a) gives (a, b, p).
+  if (warp < FAC_SEEDS) {
+    const int s = warp;
+    const uint32_t a = s_a[s], b = s_b[s];
+    if (a == FAC_NONE || b == FAC_NONE) return;
+    const uint32_t u = s >= 4 ? b : a, v = s >= 4 ? a : b;
+    Wrap W;
+    wrap_begin(W, T, u, v);
+    const uint32_t p = wrap_query(W, T, P, s_stk[s]);
+    if (s == 0 && lane == 0) {
+      C->a0 = a;
+      C->b0 = b;
+      C->init_cycles = (unsigned long long)(clock64() - t_start);
+    }
+    if (p == FAC_NONE) return;
+    fac_emit(w, T.orig, out, ws.st->facet_cap, v, u, p, -1);
+  }
 }
 
 // ------------------------------------------------------------------ F7c
-__global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FilterWs f, FacetWs w) {
+__global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FacetWs w) {
   __shared__ FilterParams sP;
   __shared__ uint32_t s_stk[FAC_BLOCK / 32][F_STACK];
-  if (threadIdx.x == 0) sP = *f.fp;
+  if (threadIdx.x == 0) sP = *w.kfp;
   __syncthreads();
   const FilterParams& P = sP;
   FacetCtl* C = w.ctl;
   int32_t* out = ws.st->out_facets;
   if (!out || P.m < 4 || C->status) return;
   const int64_t cap = ws.st->facet_cap;
-  const uint32_t* vout = ws.vout;
   const int lane = threadIdx.x & 31;
   uint32_t* stk = s_stk[threadIdx.x >> 5];
-  const FacTree T{f.sx, f.sy, f.sz, f.sid, f.keep, vout};
+  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox};
   const unsigned long long icap = C->icap, emask = C->emask;
   const uint32_t idm = (1u << FAC_ID_BITS) - 1;
+  unsigned long long st_q = 0, st_b = 0, st_bb = 0, st_n = 0, st_wrap = 0, st_wait = 0;
   for (;;) {
+    const long long t0 = clock64();
     unsigned int idx = 0;
     if (lane == 0) idx = atomicAdd(&C->head, 1u);
     idx = __shfl_sync(0xFFFFFFFFu, idx, 0);
@@ -519,7 +658,9 @@ __global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FilterWs f
       }
     }
     done = __shfl_sync(0xFFFFFFFFu, done, 0);
-    if (done) return;
+    const long long t1 = clock64();
+    st_wait += (unsigned long long)(t1 - t0);
+    if (done) break;
     item = __shfl_sync(0xFFFFFFFFu, item, 0);
     __threadfence();
     const uint32_t a = (uint32_t)(item >> FAC_ID_BITS) & idm, b = (uint32_t)item & idm;
@@ -528,20 +669,34 @@ __global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FilterWs f
     known = __shfl_sync(0xFFFFFFFFu, known, 0);
     if (!known) {
       Wrap W;
-      wrap_begin(W, f, vout, a, b);
-      const uint32_t p = wrap_query(W, T, P, f, stk);
-      if (p != FAC_NONE) fac_emit(w, vout, out, cap, b, a, p, 0);
+      wrap_begin(W, T, a, b);
+      const uint32_t p = wrap_query(W, T, P, stk);
+      if (p != FAC_NONE) fac_emit(w, T.orig, out, cap, b, a, p, 0);
+      st_q++;
+      st_b += W.nb;
+      st_bb += W.nbb;
+      st_n += W.nn;
     }
+    st_wrap += (unsigned long long)(clock64() - t1);
     __syncwarp();
     if (lane == 0) {
       __threadfence();
       atomicAdd(&C->completed, 1u);
     }
   }
+  if (lane == 0) {
+    atomicAdd(&C->queries, st_q);
+    atomicAdd(&C->batches, st_b);
+    atomicAdd(&C->beat_batches, st_bb);
+    atomicAdd(&C->nodes, st_n);
+    atomicAdd(&C->wrap_cycles, st_wrap);
+    atomicAdd(&C->wait_cycles, st_wait);
+  }
 }
 
 // ------------------------------------------------------------------ F7d
 __global__ void k_fac_done(Workspace ws, FilterWs f, FacetWs w) {
+  if (!ws.st->out_facets) return;
   if (threadIdx.x != 0) return;
   FacetCtl* C = w.ctl;
   const uint32_t nf = C->nfacets;
@@ -551,9 +706,19 @@ __global__ void k_fac_done(Workspace ws, FilterWs f, FacetWs w) {
 }
 
 static inline int facet_launch(FacetWs& w, FilterWs& f, Workspace ws, int nsm, int wrap_occ, cudaStream_t s) {
+  // the kept vertices' box tree reuses the filter's box kernels on a view
+  FilterWs kv = f;
+  kv.fp = w.kfp;
+  kv.sx = kv.cx = w.kx;
+  kv.sy = kv.cy = w.ky;
+  kv.sz = kv.cz = w.kz;
+  kv.nbox = w.knbox;
   k_fac_clear<<<nsm * 4, BLOCK, 0, s>>>(ws, f, w);
-  k_fac_init<<<1, 1024, 0, s>>>(ws, f, w);
-  k_fac_wrap<<<nsm * wrap_occ, FAC_BLOCK, 0, s>>>(ws, f, w);
+  k_fac_keep<<<1, 1024, 0, s>>>(ws, f, w);
+  k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(kv);
+  k_f_boxes_hi<<<1, 1024, 0, s>>>(kv);
+  k_fac_init<<<1, 1024, 0, s>>>(ws, w);
+  k_fac_wrap<<<nsm * wrap_occ, FAC_BLOCK, 0, s>>>(ws, w);
   k_fac_done<<<1, 32, 0, s>>>(ws, f, w);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 10;
 }

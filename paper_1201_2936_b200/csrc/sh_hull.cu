@@ -813,6 +813,17 @@ int sh_filter_stats(sh_ctx* c, int64_t* out, int64_t cap) {
   return (int)n;
 }
 
+int sh_facet_stats(sh_ctx* c, int64_t* out, int64_t cap) {
+  if (!c || !c->facws.ctl || cap <= 0) return 0;
+  FacetCtl C;
+  if (cudaMemcpy(&C, c->facws.ctl, sizeof(C), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  int64_t v[9] = {C.nfacets, C.reserved, (int64_t)C.queries, (int64_t)C.batches, (int64_t)C.beat_batches,
+                  (int64_t)C.nodes, (int64_t)C.wrap_cycles, (int64_t)C.wait_cycles, (int64_t)C.init_cycles};
+  int64_t n = std::min<int64_t>(cap, 9);
+  for (int64_t i = 0; i < n; i++) out[i] = v[i];
+  return (int)n;
+}
+
 const char* sh_last_error(void) { return g_last_error.c_str(); }
 const char* sh_version(void) { return "seghull_b200 0.1 (sm_100a)"; }
 
