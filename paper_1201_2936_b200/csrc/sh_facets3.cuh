@@ -50,6 +50,7 @@ constexpr uint32_t FAC_NONE = 0xFFFFFFFFu;
 constexpr unsigned long long FAC_EMPTY = ~0ull;
 constexpr uint32_t ST_FAC_TOO_MANY = 1;   // m >= 2^21
 constexpr uint32_t ST_FAC_OVERFLOW = 2;   // facet_cap too small
+constexpr uint32_t ST_FAC_BROKEN = 3;     // internal: table / queue capacity exceeded
 
 struct FacetCtl {
   unsigned int head, reserved, completed, nfacets;
@@ -63,6 +64,7 @@ struct FacetWs {
   double *kx, *ky, *kz;       // kept vertices in Morton order (vertex id = position)
   uint32_t* korig;            // their original point indices
   double* knbox;              // box tree over them (layout of FilterWs::nbox)
+  double* knvol;              // oriented slabs of its levels 0-1 (FilterWs::nvol)
   FilterParams* kfp;          // its parameters (m = number of kept vertices)
   unsigned long long* ftab;   // facet keys (canonical rotation of vertex ids)
   unsigned long long* etab;   // directed edge keys
@@ -92,13 +94,14 @@ static inline int facet_alloc(FacetWs& w, uint32_t mcap) {
   ok &= cudaMalloc((void**)&w.kz, (size_t)mcap * 8 + 64) == cudaSuccess;
   ok &= cudaMalloc((void**)&w.korig, (size_t)mcap * 4 + 64) == cudaSuccess;
   ok &= cudaMalloc((void**)&w.knbox, ((size_t)mcap / 31 + 2 * F_LEVELS + 8) * 48) == cudaSuccess;
+  ok &= cudaMalloc((void**)&w.knvol, ((size_t)mcap / 31 + 2 * F_LEVELS + 8) * 72) == cudaSuccess;
   ok &= cudaMalloc((void**)&w.kfp, sizeof(FilterParams)) == cudaSuccess;
   w.mcap = mcap;
   return ok ? 0 : 1;
 }
 
 static inline void facet_free(FacetWs& w) {
-  void* ps[] = {w.ftab, w.etab, w.items, w.ctl, w.kx, w.ky, w.kz, w.korig, w.knbox, w.kfp};
+  void* ps[] = {w.ftab, w.etab, w.items, w.ctl, w.kx, w.ky, w.kz, w.korig, w.knbox, w.knvol, w.kfp};
   for (void* p : ps)
     if (p) cudaFree(p);
   w = FacetWs{};
@@ -113,25 +116,30 @@ __device__ __forceinline__ unsigned long long fac_mix(unsigned long long k) {
   return k;
 }
 
-// true if newly inserted
-__device__ bool hset_insert(unsigned long long* tab, unsigned long long mask, unsigned long long key) {
+// true if newly inserted; a full table (only possible if the construction
+// went wrong) sets *status and reports the key as present
+__device__ bool hset_insert(unsigned long long* tab, unsigned long long mask, unsigned long long key,
+                            unsigned int* status) {
   unsigned long long h = fac_mix(key) & mask;
-  for (;;) {
+  for (unsigned long long probe = 0; probe <= mask; probe++) {
     const unsigned long long old = atomicCAS(&tab[h], FAC_EMPTY, key);
     if (old == FAC_EMPTY) return true;
     if (old == key) return false;
     h = (h + 1) & mask;
   }
+  atomicExch(status, ST_FAC_BROKEN);
+  return false;
 }
 
 __device__ bool hset_find(const unsigned long long* tab, unsigned long long mask, unsigned long long key) {
   unsigned long long h = fac_mix(key) & mask;
-  for (;;) {
+  for (unsigned long long probe = 0; probe <= mask; probe++) {
     const unsigned long long v = *(const volatile unsigned long long*)&tab[h];
     if (v == key) return true;
     if (v == FAC_EMPTY) return false;
     h = (h + 1) & mask;
   }
+  return true;
 }
 
 __device__ __forceinline__ unsigned long long edge_key(uint32_t u, uint32_t v) {
@@ -235,6 +243,7 @@ struct KTree {
   const double *x, *y, *z;
   const uint32_t* orig;  // original point index (output, perturbation order)
   const double* nbox;
+  const double* nvol;
 };
 
 // One 32-vertex batch (positions p = base + lane): lanes whose vertex beats
@@ -302,6 +311,16 @@ __device__ __forceinline__ bool wrap_box_may_beat(const Wrap& W, const double* b
   return !(bound < -mul(2.0 * WRAP_ERR, perm));
 }
 
+// the same test against a node's oriented slab (levels 0-1)
+__device__ __forceinline__ bool wrap_vol_may_beat(const Wrap& W, const double* vol) {
+  if (W.iq == FAC_NONE) return true;
+  const V3 n = v3(W.n[0], W.n[1], W.n[2]), q = v3(W.q[0], W.q[1], W.q[2]);
+  const double vb = vol_bound(vol, n, q);
+  const double ext = fabs(__ldg(vol + 0) - q.x) + fabs(__ldg(vol + 1) - q.y) + fabs(__ldg(vol + 2) - q.z) +
+                     __ldg(vol + 8) + fmax(fabs(__ldg(vol + 6)), fabs(__ldg(vol + 7)));
+  return !(vb < -2.0 * WRAP_ERR * (W.P[0] + W.P[1] + W.P[2]) * ext);
+}
+
 __device__ __forceinline__ void load_box(const double* src, double* bx) {
 #pragma unroll
   for (int k = 0; k < 6; k++) bx[k] = __ldg(src + k);
@@ -336,11 +355,13 @@ __device__ uint32_t wrap_query(Wrap& W, const KTree& T, const FilterParams& P, u
     double bx[6];
     load_box(T.nbox + (size_t)(P.loff[cl] + cn) * 6, bx);
     if (!wrap_box_may_beat(W, bx)) continue;
+    if (cl <= 1 && !wrap_vol_may_beat(W, T.nvol + (size_t)(P.loff[cl] + cn) * 9)) continue;
     const uint32_t chl = cl - 1, ch = cn * 32 + lane;
     bool pass = false;
     if (ch < P.lnodes[chl]) {
       load_box(T.nbox + (size_t)(P.loff[chl] + ch) * 6, bx);
-      pass = wrap_box_may_beat(W, bx);
+      pass = wrap_box_may_beat(W, bx) &&
+             (chl > 1 || wrap_vol_may_beat(W, T.nvol + (size_t)(P.loff[chl] + ch) * 9));
     }
     uint32_t mask = __ballot_sync(0xFFFFFFFFu, pass);
     if (chl == 0) {
@@ -386,7 +407,7 @@ __device__ void fac_emit(const FacetWs& w, const uint32_t* orig, int32_t* out, i
                          uint32_t y, uint32_t z, int skip) {
   if ((threadIdx.x & 31) != 0) return;
   FacetCtl* C = w.ctl;
-  if (!hset_insert(w.ftab, C->fmask, facet_key(x, y, z))) return;
+  if (!hset_insert(w.ftab, C->fmask, facet_key(x, y, z), &C->status)) return;
   const unsigned int pos = atomicAdd(&C->nfacets, 1u);
   if ((int64_t)pos < cap) {
     out[3 * (size_t)pos + 0] = (int32_t)orig[x];
@@ -394,7 +415,7 @@ __device__ void fac_emit(const FacetWs& w, const uint32_t* orig, int32_t* out, i
     out[3 * (size_t)pos + 2] = (int32_t)orig[z];
   }
   const uint32_t u[3] = {x, y, z}, v[3] = {y, z, x};
-  for (int k = 0; k < 3; k++) hset_insert(w.etab, C->emask, edge_key(u[k], v[k]));
+  for (int k = 0; k < 3; k++) hset_insert(w.etab, C->emask, edge_key(u[k], v[k]), &C->status);
   unsigned long long push[3];
   int np = 0;
   for (int k = 0; k < 3; k++) {
@@ -402,10 +423,18 @@ __device__ void fac_emit(const FacetWs& w, const uint32_t* orig, int32_t* out, i
     if (hset_find(w.etab, C->emask, edge_key(v[k], u[k]))) continue;
     push[np++] = (1ull << 63) | edge_key(u[k], v[k]);
   }
-  if (np) {
+  if (np && *(volatile unsigned int*)&C->status == 0) {
     const unsigned int base = atomicAdd(&C->reserved, (unsigned int)np);
-    for (int k = 0; k < np; k++)
+    int lost = 0;
+    for (int k = 0; k < np; k++) {
       if (base + k < C->icap) *(volatile unsigned long long*)&w.items[base + k] = push[k];
+      else lost++;
+    }
+    if (lost) {  // never written: count them as completed so the queue drains
+      atomicExch(&C->status, ST_FAC_BROKEN);
+      __threadfence();
+      atomicAdd(&C->completed, (unsigned int)lost);
+    }
   }
 }
 
@@ -492,7 +521,7 @@ __global__ void __launch_bounds__(1024) k_fac_init(Workspace ws, FacetWs w) {
   FacetCtl* C = w.ctl;
   int32_t* out = ws.st->out_facets;
   if (!out || K < 4 || C->status) return;
-  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox};
+  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox, w.knvol};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // (A) the six perturbed axis extremes
   {
@@ -630,7 +659,7 @@ __global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FacetWs w)
   const int64_t cap = ws.st->facet_cap;
   const int lane = threadIdx.x & 31;
   uint32_t* stk = s_stk[threadIdx.x >> 5];
-  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox};
+  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox, w.knvol};
   const unsigned long long icap = C->icap, emask = C->emask;
   const uint32_t idm = (1u << FAC_ID_BITS) - 1;
   unsigned long long st_q = 0, st_b = 0, st_bb = 0, st_n = 0, st_wrap = 0, st_wait = 0;
@@ -713,10 +742,12 @@ static inline int facet_launch(FacetWs& w, FilterWs& f, Workspace ws, int nsm, i
   kv.sy = kv.cy = w.ky;
   kv.sz = kv.cz = w.kz;
   kv.nbox = w.knbox;
+  kv.nvol = w.knvol;
   k_fac_clear<<<nsm * 4, BLOCK, 0, s>>>(ws, f, w);
   k_fac_keep<<<1, 1024, 0, s>>>(ws, f, w);
   k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(kv);
   k_f_boxes_hi<<<1, 1024, 0, s>>>(kv);
+  k_f_vols<<<nsm * 4, BLOCK, 0, s>>>(kv);
   k_fac_init<<<1, 1024, 0, s>>>(ws, w);
   k_fac_wrap<<<nsm * wrap_occ, FAC_BLOCK, 0, s>>>(ws, w);
   k_fac_done<<<1, 32, 0, s>>>(ws, f, w);

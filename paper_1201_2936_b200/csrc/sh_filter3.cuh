@@ -72,6 +72,7 @@ struct FilterWs {
   uint32_t* spos;                    // sorted position of discovery index
   uint32_t *cell_cnt, *cell_start, *cell_cur;
   double* nbox;                      // [node][6]: lo x,y,z, hi x,y,z (all levels)
+  double* nvol;                      // [node][9]: oriented slab of levels 0-1 (see k_f_vols)
   uint8_t* keep;
 };
 
@@ -96,13 +97,14 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
   A((void**)&f.cell_start, (cells + 1) * 4);
   A((void**)&f.cell_cur, cells * 4);
   A((void**)&f.nbox, nodes * 48);
+  A((void**)&f.nvol, nodes * 72);
   f.mcap = (uint32_t)mcap;
   return ok ? 0 : 1;
 }
 
 static inline void filter_free(FilterWs& f) {
   void* ps[] = {f.result, f.fp, f.cx, f.cy, f.cz, f.sx, f.sy, f.sz, f.ccell, f.sid, f.spos, f.keep,
-                f.cell_cnt, f.cell_start, f.cell_cur, f.nbox};
+                f.cell_cnt, f.cell_start, f.cell_cur, f.nbox, f.nvol};
   for (void* p : ps)
     if (p) cudaFree(p);
   f = FilterWs{};
@@ -423,7 +425,6 @@ __global__ void __launch_bounds__(1024) k_f_boxes_hi(FilterWs f) {
   }
 }
 
-// ------------------------------------------------------------------ F5
 struct V3 {
   double x, y, z;
 };
@@ -441,12 +442,97 @@ __device__ __forceinline__ V3 vcross(V3 u, V3 v) {
 }
 __device__ __forceinline__ V3 vneg(V3 a) { return v3(-a.x, -a.y, -a.z); }
 
+// ------------------------------------------------------------------ F4c
+// Oriented slabs for the nodes of levels 0 and 1 (32 / 1024 candidates).
+// The candidates lie near the hull surface, where an axis-aligned box
+// overestimates the support d.c by O(patch size) while a slab along the
+// patch's outward axis overestimates it by O(patch size^2) (the sagitta):
+//   c   = mean of the node's points, u = unit(c - centroid of all),
+//   [hmin, hmax] = range of u.(p - c), rho = max |(p - c) - (u.(p - c)) u|,
+//   max_p d.(p - v) <= d.(c - v) + max(a hmax, a hmin) + |d_perp| rho,
+//   a = d.u, |d_perp| = sqrt(|d|^2 - a^2).
+// Stored ranges are widened by 1e-13 of the node's extent and vol_bound
+// adds a relative margin, so the fp64 bound is >= every fp64 point value.
+__global__ void __launch_bounds__(BLOCK) k_f_vols(FilterWs f) {
+  const FilterParams* P = f.fp;
+  const uint32_t m = P->m, n0 = P->lnodes[0], n1 = P->nlev > 1 ? P->lnodes[1] : 0;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, W = (gridDim.x * blockDim.x) >> 5;
+  const double inv_m = m ? 1.0 / (double)m : 0.0;
+  const V3 G = v3(P->gsum[0] * inv_m, P->gsum[1] * inv_m, P->gsum[2] * inv_m);
+  for (uint32_t node = gw; node < n0 + n1; node += W) {
+    const uint32_t lev = node < n0 ? 0 : 1, j = node < n0 ? node : node - n0;
+    const uint32_t span = lev ? 1024u : 32u;
+    const uint32_t p0 = j * span, p1 = min(p0 + span, m);
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    for (uint32_t p = p0 + lane; p < p1; p += 32) {
+      sx += f.sx[p];
+      sy += f.sy[p];
+      sz += f.sz[p];
+    }
+    for (int o = 16; o; o >>= 1) {
+      sx += __shfl_xor_sync(0xFFFFFFFFu, sx, o);
+      sy += __shfl_xor_sync(0xFFFFFFFFu, sy, o);
+      sz += __shfl_xor_sync(0xFFFFFFFFu, sz, o);
+    }
+    const double inv = 1.0 / (double)(p1 - p0);
+    const V3 c = v3(sx * inv, sy * inv, sz * inv);
+    V3 u = vsub(c, G);
+    double ul = sqrt_(vdot(u, u));
+    if (!(ul > 0.0)) {
+      u = v3(1.0, 0.0, 0.0);
+      ul = 1.0;
+    }
+    u = v3(u.x / ul, u.y / ul, u.z / ul);
+    double hmin = INFINITY, hmax = -INFINITY, rho = 0.0, wmax = 0.0;
+    for (uint32_t p = p0 + lane; p < p1; p += 32) {
+      const V3 w = vsub(v3(f.sx[p], f.sy[p], f.sz[p]), c);
+      const double h = vdot(u, w);
+      const V3 t = vsub(w, vscale(u, h));
+      hmin = fmin(hmin, h);
+      hmax = fmax(hmax, h);
+      rho = fmax(rho, sqrt_(vdot(t, t)));
+      wmax = fmax(wmax, fabs(w.x) + fabs(w.y) + fabs(w.z));
+    }
+    for (int o = 16; o; o >>= 1) {
+      hmin = fmin(hmin, __shfl_xor_sync(0xFFFFFFFFu, hmin, o));
+      hmax = fmax(hmax, __shfl_xor_sync(0xFFFFFFFFu, hmax, o));
+      rho = fmax(rho, __shfl_xor_sync(0xFFFFFFFFu, rho, o));
+      wmax = fmax(wmax, __shfl_xor_sync(0xFFFFFFFFu, wmax, o));
+    }
+    const double slack = 1e-13 * wmax;
+    const double vals[9] = {c.x, c.y, c.z, u.x, u.y, u.z, hmin - slack, hmax + slack, rho + slack};
+    if (lane < 9) {
+      double v = vals[0];
+#pragma unroll
+      for (int k = 1; k < 9; k++) v = (lane == k) ? vals[k] : v;
+      f.nvol[(size_t)(P->loff[lev] + j) * 9 + lane] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ F5
+
 // max over the box of d.(c - v), evaluated with the point formula's order
 __device__ __forceinline__ double box_bound(const double* b, V3 d, V3 v) {
   const double t0 = fmax(mul(d.x, sub(__ldg(b + 0), v.x)), mul(d.x, sub(__ldg(b + 3), v.x)));
   const double t1 = fmax(mul(d.y, sub(__ldg(b + 1), v.y)), mul(d.y, sub(__ldg(b + 4), v.y)));
   const double t2 = fmax(mul(d.z, sub(__ldg(b + 2), v.z)), mul(d.z, sub(__ldg(b + 5), v.z)));
   return add(add(t0, t1), t2);
+}
+
+// Upper bound of d.(p - v) over a node with an oriented slab (k_f_vols),
+// valid for the fp64 point values (relative margin 1e-12).
+__device__ __forceinline__ double vol_bound(const double* vol, V3 d, V3 v) {
+  const V3 c = v3(__ldg(vol + 0), __ldg(vol + 1), __ldg(vol + 2));
+  const V3 u = v3(__ldg(vol + 3), __ldg(vol + 4), __ldg(vol + 5));
+  const double hmin = __ldg(vol + 6), hmax = __ldg(vol + 7), rho = __ldg(vol + 8);
+  const V3 cv = vsub(c, v);
+  const double dc = vdot(d, cv), al = vdot(d, u), dd = vdot(d, d);
+  const double beta = sqrt_(fmax(dd - al * al, 0.0) + 1e-15 * dd);
+  const double b = dc + fmax(al * hmax, al * hmin) + beta * rho;
+  const double d1 = fabs(d.x) + fabs(d.y) + fabs(d.z);
+  return b + 1e-12 * d1 * (fabs(cv.x) + fabs(cv.y) + fabs(cv.z) + rho + fmax(fabs(hmin), fabs(hmax)));
 }
 
 struct Sup {
@@ -536,7 +622,10 @@ __device__ Sup support_query(const FilterWs& f, const FilterParams& P, V3 d, V3 
     const uint32_t chl = cl - 1;
     const uint32_t ch = cn * 32 + lane;
     double b = -INFINITY;
-    if (ch < P.lnodes[chl]) b = box_bound(f.nbox + (size_t)(P.loff[chl] + ch) * 6, d, v);
+    if (ch < P.lnodes[chl]) {
+      b = box_bound(f.nbox + (size_t)(P.loff[chl] + ch) * 6, d, v);
+      if (chl <= 1) b = fmin(b, vol_bound(f.nvol + (size_t)(P.loff[chl] + ch) * 9, d, v));
+    }
     const bool pass = first_hit ? (b > thr) : (b >= best.val && b > -INFINITY);
     uint32_t mask = __ballot_sync(0xFFFFFFFFu, pass);
     if (!mask) continue;
@@ -981,6 +1070,7 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_scatter<<<grid, BLOCK, 0, s>>>(f);
   k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(f);
   k_f_boxes_hi<<<1, 1024, 0, s>>>(f);
+  k_f_vols<<<nsm * 4, BLOCK, 0, s>>>(f);
   k_f_test<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_compact<<<1, 1024, 0, s>>>(ws, f);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 10;

@@ -438,6 +438,7 @@ static int fetch(sh_ctx* c, sh_result* res, cudaStream_t s) {
   if (c->dim == 3 && c->last_facets && h->status == ST_OK) {
     if (fres[4] == ST_FAC_TOO_MANY)
       return set_err(SH_CONTRACT, "facet output supports fewer than 2^21 candidate vertices");
+    if (fres[4] == ST_FAC_BROKEN) return set_err(SH_CUDA, "facet construction exceeded its tables (internal error)");
     if (fres[4] == ST_FAC_OVERFLOW)
       return set_err(SH_CONTRACT, "facet_cap too small: " + std::to_string(fres[1]) + " facets");
   }
