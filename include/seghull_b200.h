@@ -135,7 +135,9 @@ int64_t sh_launch_times(sh_ctx* ctx, int32_t* kind, float* ms, int64_t cap);
  * candidates kept as within-eps ambiguous, GJK iteration caps, candidates
  * certified by the first query, support queries, points scanned, GJK
  * iterations, pruned by the local GJK, certified after the local GJK,
- * resolved by the global GJK.  Returns the count written (<= cap, <= 11). */
+ * resolved by the global GJK, then SM cycles (summed over warps) spent in
+ * the first query, the local GJK, the query after it and the global GJK.
+ * Returns the count written (<= cap, <= 15). */
 int sh_filter_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
 
 /* Diagnostics of the last 3D facet build: facets, queue items, wrap

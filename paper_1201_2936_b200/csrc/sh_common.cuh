@@ -37,8 +37,14 @@ constexpr int TILE = BLOCK * ITEMS;  // 2048 points per tile
 constexpr int ITEMS3 = 4;            // children per thread per tile (bookkeeping kernel)
 constexpr int TILE3 = BLOCK * ITEMS3;
 constexpr int MAX_TRACE = 4096;      // per-round counters kept on device
-constexpr int RB = 128;              // threads per round-kernel block
-constexpr int RITEMS = 4;            // points per thread per round tile
+#ifndef SH_RB
+#define SH_RB 128
+#endif
+#ifndef SH_RITEMS
+#define SH_RITEMS 4
+#endif
+constexpr int RB = SH_RB;            // threads per round-kernel block
+constexpr int RITEMS = SH_RITEMS;    // points per thread per round tile
 constexpr int RTILE = RB * RITEMS;   // 1024 points per round tile
 constexpr int WMAX = 128;            // tile-window segments kept in shared memory
 constexpr uint32_t BOOK_SMALL = 1024; // children handled by a single K3 block

@@ -59,6 +59,7 @@ struct FilterParams {
   uint32_t ambiguous, gjk_capped, pad0, pad1;
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
   unsigned long long local_in, local_out, fallback;
+  unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;  // SM cycles per phase (summed over warps)
 };
 
 struct FilterWs {
@@ -113,6 +114,7 @@ static inline void filter_free(FilterWs& f) {
 // per-warp diagnostics (every lane holds the same values)
 struct FStat {
   unsigned long long scanned, queries, iters, certified, local_in, local_out, fallback;
+  unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;
 };
 
 __device__ __forceinline__ unsigned long long obits(double d) { return ordered_bits(d); }
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
     P->local_in = 0;
     P->local_out = 0;
     P->fallback = 0;
+    P->cyc_cert = P->cyc_local = P->cyc_out = P->cyc_fallback = 0;
     // box tree: level 0 = chunks of 32 candidates, level l+1 = 32 level-l nodes
     uint32_t nl = m ? (m + 31) / 32 : 0, off = 0, lev = 0;
     for (int l = 0; l < F_LEVELS; l++) {
@@ -261,42 +264,40 @@ __global__ void __launch_bounds__(BLOCK) k_f_count(Workspace ws, FilterWs f) {
 
 // ------------------------------------------------------------------ F3
 __global__ void __launch_bounds__(1024) k_f_scan(FilterWs f) {
+  // one block; every thread scans a contiguous chunk of cells (up to 256
+  // for G = 64), chunk totals are scanned across the block
   __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_carry;
   const uint32_t G = f.fp->G;
   const uint32_t cells = G * G * G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < cells; base += 1024) {
-    uint32_t c = base + threadIdx.x;
-    uint32_t v = c < cells ? f.cell_cnt[c] : 0u;
-    uint32_t x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_w[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = s_w[lane], y = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
-        if (lane >= o) y += z;
-      }
-      s_w[lane] = y - w;
-    }
-    __syncthreads();
-    uint32_t ex = s_carry + s_w[warp] + x - v;
-    if (c < cells) {
-      f.cell_start[c] = ex;
-      f.cell_cur[c] = ex;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = ex + v;
-    __syncthreads();
+  const uint32_t chunk = (cells + 1023) / 1024;
+  const uint32_t c0 = min(threadIdx.x * chunk, cells), c1 = min(c0 + chunk, cells);
+  uint32_t tot = 0;
+  for (uint32_t c = c0; c < c1; c++) tot += f.cell_cnt[c];
+  uint32_t x = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
   }
-  if (threadIdx.x == 0) f.cell_start[cells] = s_carry;
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = s_w[lane];
+    uint32_t y = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
+      if (lane >= o) y += z;
+    }
+    s_w[lane] = y - w;
+  }
+  __syncthreads();
+  uint32_t run = s_w[warp] + x - tot;
+  for (uint32_t c = c0; c < c1; c++) {
+    f.cell_start[c] = run;
+    f.cell_cur[c] = run;
+    run += f.cell_cnt[c];
+  }
+  if (threadIdx.x == 1023) f.cell_start[cells] = run;
 }
 
 // ------------------------------------------------------------------ F4
@@ -843,7 +844,10 @@ __device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters) {
   return GJK_CAPPED;
 }
 
-constexpr int F_LOCAL = 3;  // local set: 3 * 32 sorted neighbours of the candidate
+#ifndef F_LOCAL_N
+#define F_LOCAL_N 6
+#endif
+constexpr int F_LOCAL = F_LOCAL_N;  // local set: F_LOCAL * 32 sorted neighbours of the candidate
 
 // 1 keep, 0 prune; *amb set when kept only because v is within eps of the
 // boundary of the other candidates' hull (or the iteration cap was hit).
@@ -858,7 +862,13 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   }
   // (0) certificate along v - centre (one existence query)
   const double thr0 = mul(eps, wl);
+  long long tc = clock64();
   const Sup s0 = support_query(f, P, w0, v, i, thr0, true, stk, fs);
+  {
+    const long long t2 = clock64();
+    fs.cyc_cert += (unsigned long long)(t2 - tc);
+    tc = t2;
+  }
   if (!(s0.val > thr0)) {
     fs.certified++;
     return 1;
@@ -936,6 +946,11 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
     V3 sep = w0;
     const int r = gjk(local_sup, first, eps, &sep, &iters);
     fs.iters += iters;
+    {
+      const long long t2 = clock64();
+      fs.cyc_local += (unsigned long long)(t2 - tc);
+      tc = t2;
+    }
     if (r == GJK_INSIDE) {
       fs.local_in++;
       return 0;  // strictly inside the hull of other candidates
@@ -944,6 +959,11 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
       // (2) separated from the local set along sep: one global existence query
       const double thr = mul(eps, sqrt_(vdot(sep, sep)));
       const Sup c = support_query(f, P, sep, v, i, thr, true, stk, fs);
+      {
+        const long long t2 = clock64();
+        fs.cyc_out += (unsigned long long)(t2 - tc);
+        tc = t2;
+      }
       if (!(c.val > thr)) {
         fs.local_out++;
         return 1;  // no candidate above the plane: extreme
@@ -951,6 +971,11 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
     }
   }
   fs.fallback++;
+  struct CycGuard {
+    FStat& s;
+    long long t;
+    __device__ ~CycGuard() { s.cyc_fallback += (unsigned long long)(clock64() - t); }
+  } guard{fs, clock64()};
   // (3) global GJK, started from the candidate farthest along v - centre
   const Sup s = support_query(f, P, w0, v, i, 0.0, false, stk, fs);
   if (s.pos == 0xFFFFFFFFu) return 1;
@@ -991,7 +1016,7 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 4) k_f_test(Workspace ws, Filter
   const int lane = threadIdx.x & 31;
   FStack& stk = s_stk[threadIdx.x >> 5];
   int amb_count = 0, cap_count = 0;
-  FStat fs = {0, 0, 0, 0, 0, 0, 0};
+  FStat fs = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (;;) {
     // candidates in Morton order: warps of a block work on nearby candidates
     // and share the tree nodes they touch in L1
@@ -1019,6 +1044,10 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 4) k_f_test(Workspace ws, Filter
     atomicAdd(&f.fp->local_in, fs.local_in);
     atomicAdd(&f.fp->local_out, fs.local_out);
     atomicAdd(&f.fp->fallback, fs.fallback);
+    atomicAdd(&f.fp->cyc_cert, fs.cyc_cert);
+    atomicAdd(&f.fp->cyc_local, fs.cyc_local);
+    atomicAdd(&f.fp->cyc_out, fs.cyc_out);
+    atomicAdd(&f.fp->cyc_fallback, fs.cyc_fallback);
   }
 }
 

@@ -25,6 +25,7 @@
 #include "sh_kernels.cuh"
 #include "sh_prims.cuh"
 #include "sh_round.cuh"
+#include "sh_round1.cuh"
 
 using namespace sh;
 
@@ -58,6 +59,7 @@ struct sh_ctx {
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[4];
   int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0, round1_occ2 = 0, round1_occ3 = 0;
+  int lean1_occ2 = 1, lean1_occ3 = 1;  // k_round1 blocks per SM
   uint32_t last_n = 0;
   bool last_facets = false;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
@@ -260,7 +262,14 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   // round 1 re-reads the input and applies the first split on the fly, so
   // the split's survivors are never written
   prof_begin(c, s);
-  k_round<DIM, MODE_ROUND1><<<ws.round1_grid, RB, dsm, s>>>(ws);
+#ifndef SH_LEAN_R1
+#define SH_LEAN_R1 1
+#endif
+  if (SH_LEAN_R1) {
+    k_round1<DIM><<<c->nsm * (DIM == 2 ? c->lean1_occ2 : c->lean1_occ3), R1B, 0, s>>>(ws);
+  } else {
+    k_round<DIM, MODE_ROUND1><<<ws.round1_grid, RB, dsm, s>>>(ws);
+  }
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
   prof_begin(c, s);
@@ -520,7 +529,11 @@ int sh_create(int device, sh_ctx** out) {
   c->round1_occ3 = std::max(1, o3b);
   int ob2 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
-  int of = 0;
+  int of = 0, l2 = 0, l3 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l2, k_round1<2>, R1B, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, k_round1<3>, R1B, 0);
+  c->lean1_occ2 = std::max(1, l2);
+  c->lean1_occ3 = std::max(1, l3);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_fac_wrap, FAC_BLOCK, 0);
   c->fac_occ = std::max(1, of);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob2, k_book<2>, BLOCK, 0);
@@ -806,10 +819,11 @@ int sh_filter_stats(sh_ctx* c, int64_t* out, int64_t cap) {
   if (!c || !c->fws.fp || cap <= 0) return 0;
   FilterParams P;
   if (cudaMemcpy(&P, c->fws.fp, sizeof(P), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
-  int64_t v[11] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
+  int64_t v[15] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
                    (int64_t)P.scanned, (int64_t)P.gjk_iters, (int64_t)P.local_in, (int64_t)P.local_out,
-                   (int64_t)P.fallback};
-  int64_t n = std::min<int64_t>(cap, 11);
+                   (int64_t)P.fallback, (int64_t)P.cyc_cert, (int64_t)P.cyc_local, (int64_t)P.cyc_out,
+                   (int64_t)P.cyc_fallback};
+  int64_t n = std::min<int64_t>(cap, 15);
   for (int64_t i = 0; i < n; i++) out[i] = v[i];
   return (int)n;
 }

@@ -21,14 +21,16 @@ for kind, n in [("unit-cube", 10_000_000), ("uniform-ball", 10_000_000), ("unifo
     kinds = np.zeros(4096, np.int32); ms = np.zeros(4096, np.float32)
     k = L.sh_launch_times(ctx, kinds.ctypes.data, ms.ctypes.data, 4096)
     L.sh_set_launch_mode(ctx, 0)
-    st = np.zeros(11, np.int64)
-    L.sh_filter_stats(ctx, st.ctypes.data, 11)
+    st = np.zeros(15, np.int64)
+    L.sh_filter_stats(ctx, st.ctypes.data, 15)
     tr = P.trace()
     by = {names[i]: round(float(ms[:k][kinds[:k] == i].sum()), 3) for i in sorted(set(kinds[:k].tolist()))}
     rounds = [round(float(x), 3) for x in ms[:k][kinds[:k] == 4]]
     print(f"{kind} {n}: h={idx.numel()} {by}")
     print("  rounds ms:", rounds)
     print("  trace (live, kept, nseg):", tr[:, :3].tolist())
-    print("  filter m=%d G=%d amb=%d capped=%d certified=%d queries=%d scanned=%d gjk_iters=%d local_in=%d local_out=%d fallback=%d" % tuple(st))
+    print("  filter m=%d G=%d amb=%d capped=%d certified=%d queries=%d scanned=%d gjk_iters=%d local_in=%d local_out=%d fallback=%d" % tuple(st[:11]))
+    cy = st[11:15].astype(float)
+    print("  cycles: cert %.3g local %.3g out %.3g fallback %.3g  (per cand: cert %.0f)" % (*cy, cy[0] / max(st[0], 1)))
     del d
     torch.cuda.empty_cache()
