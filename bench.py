@@ -402,7 +402,7 @@ def main():
         tot_round, tot_all, rt = best
         launches = len(round_bytes)
         achieved = sum(round_bytes) / launches / (tot_round / launches / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_round (fused round: discard+classify+regroup+argmax)",
+        roofline = {"bound": "hbm", "kernel": "k_round1 (round 1, fused with the first split) + k_round (rounds >= 2): discard+classify+regroup+argmax",
                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": committed_traffic(args.config),
                     "peak_source": peak_src, "launches": launches,
