@@ -147,6 +147,15 @@ int sh_filter_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
  * count written (<= cap, <= 9). */
 int sh_facet_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
 
+/* ---- point sources ----
+ * Device-side generation of the uniform-box benchmark clouds ("unit
+ * square" 2D / "unit cube" 3D; reference splitmix64 stream, datagen.py:
+ * 53-71): n points, global indices start..start+n-1 of the seeded cloud,
+ * bit-identical to the host generator.  layout 0: structure of arrays
+ * (out[c*n + i]); 1: rows (out[i*dim + c]).  Stream-ordered. */
+int sh_uniform_points(sh_ctx* ctx, int dim, int64_t n, uint64_t seed, int64_t start, int layout, double* out,
+                      void* stream);
+
 /* ---- framework primitives (device arrays) ----
  * Replace segments.segmented_scan (segments.py:201-234), flag_permute
  * (primitives.py:91-117), compact (:120-148) and scatter (:151-176).

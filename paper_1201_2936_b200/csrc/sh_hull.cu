@@ -20,6 +20,7 @@
 
 #include "../../include/seghull_b200.h"
 #include "sh_book.cuh"
+#include "sh_datagen.cuh"
 #include "sh_facets3.cuh"
 #include "sh_filter3.cuh"
 #include "sh_kernels.cuh"
@@ -685,6 +686,19 @@ int sh_bbox(sh_ctx* c, const double* x, const double* y, const double* z, int64_
   k_bbox_init<<<1, 32, 0, s>>>(c->bbox_bits, dim);
   k_bbox<<<c->nsm * 8, BLOCK, 0, s>>>(x, y, dim == 3 ? z : y, stride, (uint32_t)n, dim, c->bbox_bits);
   k_bbox_final<<<1, 32, 0, s>>>(c->bbox_bits, out, dim);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_uniform_points(sh_ctx* c, int dim, int64_t n, uint64_t seed, int64_t start, int layout, double* out,
+                      void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if ((dim != 2 && dim != 3) || n < 0 || start < 0 || (layout != 0 && layout != 1) || (n > 0 && !out))
+    return set_err(SH_CONTRACT, "bad uniform_points arguments");
+  if (n == 0) return SH_OK;
+  CK(cudaSetDevice(c->device));
+  k_uniform_points<<<c->nsm * 8, BLOCK, 0, (cudaStream_t)stream>>>(dim, (uint64_t)n, (unsigned long long)seed,
+                                                                 (uint64_t)start, out, layout);
   CK(cudaGetLastError());
   return SH_OK;
 }
