@@ -359,7 +359,10 @@ def main():
     value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
     # init, first reduce, first-split count, book, then (round, book) per
     # round, then output (2D) or line-far + 9 filter kernels (3D)
-    launches_per_hull = 5 + 2 * rounds + (9 if dim == 3 else 0) + (4 if want_fac else 0)
+    # + one unused launch per peeled round (k_round_long / k_round pair,
+    # rounds 2..4 outside the WHILE node), + 1 slab kernel in the 3D filter
+    peeled = max(0, min(3, rounds - 1))
+    launches_per_hull = 5 + 2 * rounds + peeled + (10 if dim == 3 else 0) + (8 if want_fac else 0)
 
     # ---------------- per-kernel pass (events after every launch)
     tr = P.trace(local)

@@ -209,6 +209,7 @@ struct Workspace {
   uint32_t max_tiles;     // round tiles at capacity
   cudaGraphConditionalHandle cond;
   uint32_t use_cond;
+  uint32_t peeled;        // launch outside the WHILE loop (first rounds): k_round_long may take the round
 };
 
 // ---------------------------------------------------------------- helpers

@@ -25,8 +25,8 @@
 #include "sh_filter3.cuh"
 #include "sh_kernels.cuh"
 #include "sh_prims.cuh"
-#include "sh_round.cuh"
 #include "sh_round1.cuh"
+#include "sh_round.cuh"
 
 using namespace sh;
 
@@ -61,6 +61,7 @@ struct sh_ctx {
   Graph g[4];
   int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0, round1_occ2 = 0, round1_occ3 = 0;
   int lean1_occ2 = 1, lean1_occ3 = 1;  // k_round1 blocks per SM
+  int long_occ2 = 1, long_occ3 = 1;    // k_round_long blocks per SM
   uint32_t last_n = 0;
   bool last_facets = false;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
@@ -224,7 +225,10 @@ static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min, uint32
 template <int DIM>
 static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   size_t dsm = RoundSmem<DIM>::bytes();
+  // exactly one of the two round kernels does the work (long_round())
   prof_begin(c, s);
+  if (SH_LEAN_LONG && ws.peeled)
+    k_round_long<DIM><<<c->nsm * (DIM == 2 ? c->long_occ2 : c->long_occ3), R1B, 0, s>>>(ws);
   k_round<DIM, MODE_NORMAL><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
@@ -320,6 +324,11 @@ static int build_graph(sh_ctx* c, bool facets = false) {
   ws.cond = handle;
   ws.use_cond = 1;
   int rc = launch_pre<DIM>(c, ws, s);
+  for (int r = 0; rc == SH_OK && SH_LEAN_LONG && r < LONG_PEEL; r++) {
+    Workspace wp = ws;
+    wp.peeled = 1;
+    rc = launch_body<DIM>(c, wp, s);
+  }
   if (rc) {
     cudaGraph_t tmp;
     cudaStreamEndCapture(s, &tmp);
@@ -410,11 +419,13 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     c->prof_n = 0;
     rc = launch_pre<DIM>(c, ws, s);
     if (rc) return rc;
-    for (;;) {
+    for (int r = 0;; r++) {
       CK(cudaMemcpyAsync(&h->rp, &c->ws.st->rp, sizeof(RoundParams), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (!h->rp.active) break;
-      rc = launch_body<DIM>(c, ws, s);
+      Workspace wr = ws;
+      wr.peeled = (SH_LEAN_LONG && r < LONG_PEEL) ? 1u : 0u;
+      rc = launch_body<DIM>(c, wr, s);
       if (rc) return rc;
     }
     rc = launch_post<DIM>(c, ws, s, want_facets);
@@ -533,6 +544,11 @@ int sh_create(int device, sh_ctx** out) {
   int of = 0, l2 = 0, l3 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l2, k_round1<2>, R1B, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, k_round1<3>, R1B, 0);
+  int g2 = 0, g3 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g2, k_round_long<2>, R1B, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g3, k_round_long<3>, R1B, 0);
+  c->long_occ2 = std::max(1, g2);
+  c->long_occ3 = std::max(1, g3);
   c->lean1_occ2 = std::max(1, l2);
   c->lean1_occ3 = std::max(1, l3);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_fac_wrap, FAC_BLOCK, 0);
