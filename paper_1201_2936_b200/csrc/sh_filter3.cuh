@@ -45,6 +45,9 @@ constexpr int FG_MAX = 64;   // grid cells per axis (max, power of two)
 constexpr int F_LEVELS = 6;  // box-tree levels: 32^6 candidates max
 constexpr int F_TEST_BLOCK = 128;
 constexpr int F_STACK = 32 * F_LEVELS;  // traversal stack entries per warp
+#ifndef SH_FGRID_SLACK
+#define SH_FGRID_SLACK 2.0
+#endif
 #ifndef F_PER_CELL
 #define F_PER_CELL 1.0   // target candidates per grid cell
 #endif
@@ -112,6 +115,14 @@ static inline void filter_free(FilterWs& f) {
 }
 
 // per-warp diagnostics (every lane holds the same values)
+// per-phase cycle counters cost ~20% of the filter: compiled in only with
+// -DSH_FILTER_CYCLES (diagnostics, sh_filter_stats)
+#ifdef SH_FILTER_CYCLES
+#define FCLK() clock64()
+#else
+#define FCLK() 0ll
+#endif
+
 struct FStat {
   unsigned long long scanned, queries, iters, certified, local_in, local_out, fallback;
   unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;
@@ -121,10 +132,11 @@ __device__ __forceinline__ unsigned long long obits(double d) { return ordered_b
 __device__ __forceinline__ double ofrom(unsigned long long b) { return from_ordered_bits(b); }
 
 __device__ __forceinline__ uint32_t f_grid_of(uint32_t m) {
-  // ~F_PER_CELL candidates per cell, G a power of two
-  double g = cbrt((double)m / F_PER_CELL);
+  // G a power of two with G^3 <= m / F_PER_CELL * SH_FGRID_SLACK (>= ~0.5
+  // candidates per cell): finer grids only cost scan time
+  double g = (double)m / F_PER_CELL * SH_FGRID_SLACK;
   uint32_t G = 2;
-  while (G < FG_MAX && (double)G < g) G <<= 1;
+  while (G < FG_MAX && (double)(2 * G) * (2 * G) * (2 * G) <= g) G <<= 1;
   return G;
 }
 
@@ -264,40 +276,65 @@ __global__ void __launch_bounds__(BLOCK) k_f_count(Workspace ws, FilterWs f) {
 
 // ------------------------------------------------------------------ F3
 __global__ void __launch_bounds__(1024) k_f_scan(FilterWs f) {
-  // one block; every thread scans a contiguous chunk of cells (up to 256
-  // for G = 64), chunk totals are scanned across the block
+  // one block; tiles of 1024 x 8 cells, each thread 8 consecutive cells
+  // (two 16-byte loads, coalesced across the block; G^3 is a multiple of 8)
   __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
   const uint32_t G = f.fp->G;
   const uint32_t cells = G * G * G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t chunk = (cells + 1023) / 1024;
-  const uint32_t c0 = min(threadIdx.x * chunk, cells), c1 = min(c0 + chunk, cells);
-  uint32_t tot = 0;
-  for (uint32_t c = c0; c < c1; c++) tot += f.cell_cnt[c];
-  uint32_t x = tot;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_w[warp] = x;
+  if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = s_w[lane];
-    uint32_t y = w;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
-      if (lane >= o) y += z;
+  for (uint32_t base = 0; base < cells; base += 8192) {
+    const uint32_t c = base + 8 * threadIdx.x;
+    uint32_t v[8];
+    if (c < cells) {
+      const uint4 a = *reinterpret_cast<const uint4*>(f.cell_cnt + c);
+      const uint4 b = *reinterpret_cast<const uint4*>(f.cell_cnt + c + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] = 0;
     }
-    s_w[lane] = y - w;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) tot += v[k];
+    uint32_t x = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t w = s_w[lane];
+      uint32_t y = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
+        if (lane >= o) y += z;
+      }
+      s_w[lane] = y - w;
+    }
+    __syncthreads();
+    uint32_t run = s_carry + s_w[warp] + x - tot;
+    if (c < cells) {
+      uint32_t o[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        o[k] = run;
+        run += v[k];
+      }
+      *reinterpret_cast<uint4*>(f.cell_start + c) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(f.cell_start + c + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+      *reinterpret_cast<uint4*>(f.cell_cur + c) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(f.cell_cur + c + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = run;
+    __syncthreads();
   }
-  __syncthreads();
-  uint32_t run = s_w[warp] + x - tot;
-  for (uint32_t c = c0; c < c1; c++) {
-    f.cell_start[c] = run;
-    f.cell_cur[c] = run;
-    run += f.cell_cnt[c];
-  }
-  if (threadIdx.x == 1023) f.cell_start[cells] = run;
+  if (threadIdx.x == 0) f.cell_start[cells] = s_carry;
 }
 
 // ------------------------------------------------------------------ F4
@@ -862,10 +899,10 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   }
   // (0) certificate along v - centre (one existence query)
   const double thr0 = mul(eps, wl);
-  long long tc = clock64();
+  long long tc = FCLK();
   const Sup s0 = support_query(f, P, w0, v, i, thr0, true, stk, fs);
   {
-    const long long t2 = clock64();
+    const long long t2 = FCLK();
     fs.cyc_cert += (unsigned long long)(t2 - tc);
     tc = t2;
   }
@@ -947,7 +984,7 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
     const int r = gjk(local_sup, first, eps, &sep, &iters);
     fs.iters += iters;
     {
-      const long long t2 = clock64();
+      const long long t2 = FCLK();
       fs.cyc_local += (unsigned long long)(t2 - tc);
       tc = t2;
     }
@@ -960,7 +997,7 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
       const double thr = mul(eps, sqrt_(vdot(sep, sep)));
       const Sup c = support_query(f, P, sep, v, i, thr, true, stk, fs);
       {
-        const long long t2 = clock64();
+        const long long t2 = FCLK();
         fs.cyc_out += (unsigned long long)(t2 - tc);
         tc = t2;
       }
@@ -974,8 +1011,8 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   struct CycGuard {
     FStat& s;
     long long t;
-    __device__ ~CycGuard() { s.cyc_fallback += (unsigned long long)(clock64() - t); }
-  } guard{fs, clock64()};
+    __device__ ~CycGuard() { s.cyc_fallback += (unsigned long long)(FCLK() - t); }
+  } guard{fs, FCLK()};
   // (3) global GJK, started from the candidate farthest along v - centre
   const Sup s = support_query(f, P, w0, v, i, 0.0, false, stk, fs);
   if (s.pos == 0xFFFFFFFFu) return 1;
@@ -1003,7 +1040,10 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   return 1;
 }
 
-__global__ void __launch_bounds__(F_TEST_BLOCK, 4) k_f_test(Workspace ws, FilterWs f) {
+#ifndef SH_FTEST_MINB
+#define SH_FTEST_MINB 3
+#endif
+__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspace ws, FilterWs f) {
   __shared__ FilterParams sP;
   __shared__ FStack s_stk[F_TEST_BLOCK / 32];
   if (threadIdx.x == 0) sP = *f.fp;
