@@ -23,7 +23,10 @@
 //   so coplanar vertices (cube corners) still give a valid triangulation.
 //
 //   F7a k_fac_clear  reset the hash tables / work queue for this m
-//   F7b k_fac_init   a0 = the vertex of minimal perturbed x; b0 = its
+//   F7b' k_fac_seeds 64 direction seeds (fp64 extreme vertex + virtual
+//                    line, facet verified exactly), see below
+//   F7b k_fac_init   (only if no direction seed survived)
+//                    a0 = the vertex of minimal perturbed x; b0 = its
 //                    neighbour on the 2D hull of the xy projection (exact
 //                    orient2d with the same perturbation, so (a0, b0) is a
 //                    3D hull edge); first facet = wrap(a0, b0) against the
@@ -333,7 +336,7 @@ __device__ uint32_t wrap_query(Wrap& W, const KTree& T, const FilterParams& P, u
   // (1) the Morton neighbourhoods of a and b
 #pragma unroll 1
   for (int k = 0; k < 4; k++) {
-    const uint32_t c = (k < 2) ? W.ia : W.ib;
+    const uint32_t c = (k < 2 || W.ib == FAC_NONE) ? W.ia : W.ib;  // ib: virtual in seeding
     const uint32_t lo = c >= 32 ? c - 32 : 0;
     wrap_batch(W, T, K, lo + (k & 1) * 32 + lane);
   }
@@ -520,7 +523,9 @@ __global__ void __launch_bounds__(1024) k_fac_init(Workspace ws, FacetWs w) {
   const uint32_t K = P.m;
   FacetCtl* C = w.ctl;
   int32_t* out = ws.st->out_facets;
-  if (!out || K < 4 || C->status) return;
+  // runs after k_fac_seeds: only needed when no direction seed survived its
+  // verification (tiny or degenerate vertex sets)
+  if (!out || K < 4 || C->status || C->nfacets) return;
   const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox, w.knvol};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // (A) the six perturbed axis extremes
@@ -646,6 +651,95 @@ __global__ void __launch_bounds__(1024) k_fac_init(Workspace ws, FacetWs w) {
   }
 }
 
+// ------------------------------------------------------------------ F7b'
+// More seeds, spread over the sphere of directions, to shorten the BFS (its
+// critical path is the number of dependent wraps from the nearest seed).
+// One warp per direction d (Fibonacci sphere):
+//   v = the fp64 argmax of d.p over the kept vertices (an extreme vertex);
+//   wrap(v, v + L e) with e a unit vector orthogonal to d and v + L e a
+//   virtual point (perturbation index -1): the plane through the line
+//   supports the hull at v, so the wrap yields a hull edge (v, p);
+//   wrap(v, p) then yields the facet (p, v, q).
+// The argmax is not exact, so the facet is verified exactly before it is
+// used: a second descent starting from q must not find any vertex beating q
+// (with q fixed the pruning is exact).  Failed seeds are dropped.
+constexpr int FAC_DIR_SEEDS = 64;
+
+__global__ void __launch_bounds__(128) k_fac_seeds(Workspace ws, FilterWs f, FacetWs w) {
+  __shared__ FilterParams sP;
+  __shared__ uint32_t s_stk[4][F_STACK];
+  if (threadIdx.x == 0) sP = *w.kfp;
+  __syncthreads();
+  const FilterParams& P = sP;
+  const uint32_t K = P.m;
+  FacetCtl* C = w.ctl;
+  int32_t* out = ws.st->out_facets;
+  if (!out || K < 4 || C->status) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t sd = blockIdx.x * 4 + warp;
+  if (sd >= (uint32_t)FAC_DIR_SEEDS) return;
+  const KTree T{w.kx, w.ky, w.kz, w.korig, w.knbox, w.knvol};
+  // direction sd of a Fibonacci sphere
+  const double zc = 1.0 - (2.0 * sd + 1.0) / FAC_DIR_SEEDS;
+  const double rr = sqrt(fmax(0.0, 1.0 - zc * zc));
+  const double ph = 2.399963229728653 * sd;
+  const double d[3] = {rr * cos(ph), rr * sin(ph), zc};
+  // fp64 argmax of d.p
+  double bv = -INFINITY;
+  uint32_t bi = FAC_NONE;
+  for (uint32_t i = lane; i < K; i += 32) {
+    const double v = d[0] * __ldg(&T.x[i]) + d[1] * __ldg(&T.y[i]) + d[2] * __ldg(&T.z[i]);
+    if (v > bv) {
+      bv = v;
+      bi = i;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+    const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  const uint32_t v = bi;
+  if (v == FAC_NONE) return;
+  // e orthogonal to d, scaled to the candidates' extent
+  double e[3];
+  {
+    const double ax[3] = {fabs(d[0]) < 0.9 ? 1.0 : 0.0, fabs(d[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+    e[0] = d[1] * ax[2] - d[2] * ax[1];
+    e[1] = d[2] * ax[0] - d[0] * ax[2];
+    e[2] = d[0] * ax[1] - d[1] * ax[0];
+    double span = 0.0;
+    for (int k = 0; k < 3; k++)
+      span = fmax(span, from_ordered_bits(f.fp->bb[3 + k]) - from_ordered_bits(f.fp->bb[k]));
+    const double el = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+    for (int k = 0; k < 3; k++) e[k] = e[k] / el * (span > 0.0 ? span : 1.0);
+  }
+  uint32_t* stk = s_stk[warp];
+  Wrap W;
+  wrap_begin(W, T, v, v);
+  W.ib = FAC_NONE;  // virtual second point v + e
+  W.gb = -1;
+  W.b[0] = W.a[0] + e[0];
+  W.b[1] = W.a[1] + e[1];
+  W.b[2] = W.a[2] + e[2];
+  const uint32_t p = wrap_query(W, T, P, stk);
+  if (p == FAC_NONE) return;
+  wrap_begin(W, T, v, p);
+  const uint32_t q = wrap_query(W, T, P, stk);
+  if (q == FAC_NONE) return;
+  // exact verification: nothing beats q for the edge (v, p)
+  wrap_begin(W, T, v, p);
+  {
+    double qq[3] = {T.x[q], T.y[q], T.z[q]};
+    wrap_set_q(W, q, (int64_t)T.orig[q], qq);
+  }
+  if (wrap_query(W, T, P, stk) != q) return;
+  fac_emit(w, T.orig, out, ws.st->facet_cap, p, v, q, -1);
+}
+
 // ------------------------------------------------------------------ F7c
 __global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FacetWs w) {
   __shared__ FilterParams sP;
@@ -748,6 +842,7 @@ static inline int facet_launch(FacetWs& w, FilterWs& f, Workspace ws, int nsm, i
   k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(kv);
   k_f_boxes_hi<<<1, 1024, 0, s>>>(kv);
   k_f_vols<<<nsm * 4, BLOCK, 0, s>>>(kv);
+  k_fac_seeds<<<(FAC_DIR_SEEDS + 3) / 4, 128, 0, s>>>(ws, f, w);
   k_fac_init<<<1, 1024, 0, s>>>(ws, w);
   k_fac_wrap<<<nsm * wrap_occ, FAC_BLOCK, 0, s>>>(ws, w);
   k_fac_done<<<1, 32, 0, s>>>(ws, f, w);
