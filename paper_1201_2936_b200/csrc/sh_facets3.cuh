@@ -663,7 +663,10 @@ __global__ void __launch_bounds__(1024) k_fac_init(Workspace ws, FacetWs w) {
 // The argmax is not exact, so the facet is verified exactly before it is
 // used: a second descent starting from q must not find any vertex beating q
 // (with q fixed the pruning is exact).  Failed seeds are dropped.
-constexpr int FAC_DIR_SEEDS = 64;
+#ifndef SH_FAC_SEEDS
+#define SH_FAC_SEEDS 256
+#endif
+constexpr int FAC_DIR_SEEDS = SH_FAC_SEEDS;
 
 __global__ void __launch_bounds__(128) k_fac_seeds(Workspace ws, FilterWs f, FacetWs w) {
   __shared__ FilterParams sP;

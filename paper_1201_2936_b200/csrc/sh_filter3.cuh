@@ -884,7 +884,11 @@ __device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters) {
 #ifndef F_LOCAL_N
 #define F_LOCAL_N 6
 #endif
-constexpr int F_LOCAL = F_LOCAL_N;  // local set: F_LOCAL * 32 sorted neighbours of the candidate
+constexpr int F_LOCAL = F_LOCAL_N;
+#ifndef SH_F_EXTRA
+#define SH_F_EXTRA 12
+#endif
+constexpr int F_EXTRA = SH_F_EXTRA;  // global points added to the local set  // local set: F_LOCAL * 32 sorted neighbours of the candidate
 
 // 1 keep, 0 prune; *amb set when kept only because v is within eps of the
 // boundary of the other candidates' hull (or the iteration cap was hit).
@@ -930,6 +934,13 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
     }
     const double inv = 1.0 / (double)(P.m - 1);
     const V3 g = vsub(v3(mul(sub(gsum.x, v.x), inv), mul(sub(gsum.y, v.y), inv), mul(sub(gsum.z, v.z), inv)), v);
+    // points found above a separating plane of the local set join it (one
+    // per lane, up to F_EXTRA) and the local GJK is rerun: most candidates
+    // the local set can not decide are settled after one or two of these
+    // existence queries instead of a global GJK
+    V3 ex_u = v3(0.0, 0.0, 0.0);
+    uint32_t ex_id = 0xFFFFFFFFu;
+    int nex = 0;
     auto local_sup = [&](V3 d) -> SupU {
       double bv = -INFINITY;
       uint32_t bid = 0xFFFFFFFFu;
@@ -951,6 +962,14 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
           bk = F_LOCAL;
         }
       }
+      if (lane < nex) {  // global points found above earlier separating planes
+        const double val = vdot(d, ex_u);
+        if (val > bv || (val == bv && ex_id < bid)) {
+          bv = val;
+          bid = ex_id;
+          bk = F_LOCAL + 1;
+        }
+      }
       int bl = lane;
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -968,6 +987,7 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
 #pragma unroll
       for (int k = 0; k < F_LOCAL; k++)
         if (kk == k) u = lu[k];
+      if (kk == F_LOCAL + 1) u = ex_u;
       SupU r;
       r.val = bv;
       r.id = bid;
@@ -981,18 +1001,21 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
     first.id = s0.id;
     first.u = vsub(v3(f.sx[s0.pos], f.sy[s0.pos], f.sz[s0.pos]), v);
     V3 sep = w0;
-    const int r = gjk(local_sup, first, eps, &sep, &iters);
-    fs.iters += iters;
-    {
-      const long long t2 = FCLK();
-      fs.cyc_local += (unsigned long long)(t2 - tc);
-      tc = t2;
-    }
-    if (r == GJK_INSIDE) {
-      fs.local_in++;
-      return 0;  // strictly inside the hull of other candidates
-    }
-    if (r == GJK_OUTSIDE) {
+#pragma unroll 1
+    for (int xr = 0; xr <= F_EXTRA; xr++) {
+      iters = 0;
+      const int r = gjk(local_sup, first, eps, &sep, &iters);
+      fs.iters += iters;
+      {
+        const long long t2 = FCLK();
+        fs.cyc_local += (unsigned long long)(t2 - tc);
+        tc = t2;
+      }
+      if (r == GJK_INSIDE) {
+        fs.local_in++;
+        return 0;  // strictly inside the hull of other candidates
+      }
+      if (r != GJK_OUTSIDE) break;
       // (2) separated from the local set along sep: one global existence query
       const double thr = mul(eps, sqrt_(vdot(sep, sep)));
       const Sup c = support_query(f, P, sep, v, i, thr, true, stk, fs);
@@ -1005,6 +1028,16 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
         fs.local_out++;
         return 1;  // no candidate above the plane: extreme
       }
+      if (xr == F_EXTRA) break;
+      const V3 cu = vsub(v3(f.sx[c.pos], f.sy[c.pos], f.sz[c.pos]), v);
+      if (lane == nex) {
+        ex_u = cu;
+        ex_id = c.id;
+      }
+      nex++;
+      first.val = c.val;
+      first.id = c.id;
+      first.u = cu;
     }
   }
   fs.fallback++;
