@@ -149,6 +149,8 @@ struct DevState {
   int64_t* out_idx;       // user output (device), capacity n
   int32_t* out_facets;    // 3D facet triples (device), NULL = not requested
   int64_t facet_cap;      // triples out_facets can hold
+  uint32_t long_min_live; // k_round_long thresholds (sh_round1.cuh; env overrides for tests)
+  uint32_t long_seg_min;
   // ---- first split (K0/K0b) ----
   double eps;
   uint32_t imin, imax, ifar;

@@ -404,6 +404,12 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
   h->eps_abs = std::isnan(eps_abs) ? 0.0 : eps_abs;
   h->segcap = c->segcap;
   h->out_idx = out_idx;
+  {
+    const char* e1 = getenv("SH_LONG_MIN_LIVE");
+    const char* e2 = getenv("SH_LONG_SEG_MIN");
+    h->long_min_live = e1 ? (uint32_t)strtoul(e1, nullptr, 10) : LONG_MIN_LIVE;
+    h->long_seg_min = e2 ? (uint32_t)strtoul(e2, nullptr, 10) : LONG_SEG_MIN;
+  }
   h->out_facets = want_facets ? facets : nullptr;
   h->facet_cap = want_facets ? facet_cap : 0;
   CK(cudaMemcpyAsync(c->ws.st, h, offsetof(DevState, eps), cudaMemcpyHostToDevice, s));

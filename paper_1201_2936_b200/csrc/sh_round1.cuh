@@ -341,8 +341,12 @@ constexpr uint32_t LONG_SEG_MIN = 4096;
 constexpr uint32_t LONG_MIN_LIVE = 4u << 20;
 constexpr int LONG_PEEL = 3;  // rounds 2..4 are launched outside the WHILE loop
 
-__device__ __forceinline__ bool long_round(const RoundParams& rp) {
-  return rp.round >= 2 && rp.n_live >= LONG_MIN_LIVE && (uint64_t)rp.n_live >= (uint64_t)LONG_SEG_MIN * rp.nseg;
+// thresholds come with the call parameters (defaults LONG_MIN_LIVE /
+// LONG_SEG_MIN; SH_LONG_MIN_LIVE / SH_LONG_SEG_MIN override them, which the
+// tests use to drive every round through this kernel)
+__device__ __forceinline__ bool long_round(const RoundParams& rp, const DevState* st) {
+  return rp.round >= 2 && rp.n_live >= st->long_min_live &&
+         (uint64_t)rp.n_live >= (uint64_t)st->long_seg_min * rp.nseg;
 }
 
 template <int DIM>
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(R1B, SH_R1_MINB) k_round_long(Workspace ws) {
   __shared__ uint32_t s_stage_i[R1B / 32][R1CHUNK];
   DevState* st = ws.st;
   const RoundParams rp = st->rp;
-  if (!ws.peeled || !rp.active || rp.root || !long_round(rp)) return;
+  if (!ws.peeled || !rp.active || rp.root || !long_round(rp, st)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (blockIdx.x == 0 && tid == 0) {
     st->ctr_book = 0;  // K3's tile counter
