@@ -128,3 +128,34 @@ def test_small_facet_cap_is_a_contract_error():
                               torch.cuda.current_stream().cuda_stream)
     assert rc == _lib.SH_CONTRACT and res.facets > 10
     assert "facet_cap" in _lib.last_error()
+
+
+def test_large_degenerate_grids():
+    # a 16^3 lattice and a 24 x 24 grid on each face of a cube: hull faces
+    # with hundreds of coplanar vertices, triangulated consistently by SoS
+    g = np.arange(16, dtype=np.float64)
+    L = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    t = np.linspace(0.0, 1.0, 24)
+    u, v = [a.ravel() for a in np.meshgrid(t, t, indexing="ij")]
+    faces = []
+    for axis in range(3):
+        for side in (0.0, 1.0):
+            f = np.empty((u.size, 3))
+            f[:, axis] = side
+            f[:, (axis + 1) % 3] = u
+            f[:, (axis + 2) % 3] = v
+            faces.append(f)
+    S = np.unique(np.concatenate(faces), axis=0)
+    for pts in (L, S):
+        idx, fac, _ = run(tuple(np.ascontiguousarray(pts.T)))
+        vset = check_mesh(fac)
+        assert set(vset.tolist()) <= set(idx.tolist())
+        check_supporting(pts, fac, exact=False)
+        # every facet's corners are coplanar with a face of the box: exact
+        # zero-volume checks are in check_supporting; the triangulated area
+        # must equal the box's surface area
+        a, b, c = pts[fac[:, 0]], pts[fac[:, 1]], pts[fac[:, 2]]
+        area = 0.5 * np.linalg.norm(np.cross(b - a, c - a), axis=1).sum()
+        span = pts.max(0) - pts.min(0)
+        want = 2 * (span[0] * span[1] + span[1] * span[2] + span[0] * span[2])
+        assert abs(area - want) <= 1e-9 * want
