@@ -74,6 +74,59 @@ __device__ __forceinline__ int classify3_bf(const Seg3& g, double qx, double qy,
 #ifndef SH_R1_MINB
 #define SH_R1_MINB 2
 #endif
+// Ranks of a warp chunk's survivors per child (key < NK; NK <= 8): rank[j]
+// = number of earlier survivors of the same child in the chunk (item-major,
+// then lane).  Returns the chunk's per-child counts packed 8 bits each
+// (child k at bit 8k; a chunk has < 256 points).  3D (6 children), per
+// item: REDUX.SUMs of the lanes' 1 << 8*key (the item's packed counts, 4
+// children per 32-bit word) and log2(NK) + 1 ballots to find the lanes with
+// the same key; 2D (4 children): one ballot per child.
+template <int NK, int ITEMS>
+__device__ __forceinline__ unsigned long long chunk_ranks(const uint32_t* key, uint32_t* rank) {
+  static_assert(NK <= 8, "8-bit fields, two 32-bit words");
+  constexpr int NBITS = NK <= 2 ? 1 : (NK <= 4 ? 2 : 3);
+  const uint32_t lt = lanemask_lt();
+  if constexpr (NK <= 4) {
+    // 2D (4 children): one ballot per child is cheaper here (measured)
+    unsigned long long packed = 0ull;
+#pragma unroll
+    for (int j = 0; j < ITEMS; j++) {
+      uint32_t r = 0;
+      unsigned long long add = 0ull;
+#pragma unroll
+      for (int k = 0; k < NK; k++) {
+        const bool mine = key[j] == (uint32_t)k;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+        r += mine ? (uint32_t)__popc(m & lt) : 0u;
+        add += (unsigned long long)__popc(m) << (8 * k);
+      }
+      const uint32_t kj = key[j] < (uint32_t)NK ? key[j] : 0u;
+      rank[j] = r + (uint32_t)((packed >> (8 * kj)) & 0xFFull);
+      packed += add;
+    }
+    return packed;
+  }
+  uint32_t run_lo = 0, run_hi = 0;
+#pragma unroll
+  for (int j = 0; j < ITEMS; j++) {
+    const uint32_t kj = key[j];
+    const bool valid = kj < (uint32_t)NK;
+    const uint32_t c_lo = __reduce_add_sync(0xFFFFFFFFu, (valid && kj < 4u) ? (1u << (8 * kj)) : 0u);
+    const uint32_t c_hi = NK > 4 ? __reduce_add_sync(0xFFFFFFFFu, (valid && kj >= 4u) ? (1u << (8 * (kj - 4))) : 0u) : 0u;
+    uint32_t grp = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+    for (int b = 0; b < NBITS; b++) {
+      const uint32_t mb = __ballot_sync(0xFFFFFFFFu, (kj >> b) & 1u);
+      grp &= ((kj >> b) & 1u) ? mb : ~mb;
+    }
+    const uint32_t base = kj < 4u ? (run_lo >> (8 * kj)) & 0xFFu : (run_hi >> (8 * ((kj - 4) & 3u))) & 0xFFu;
+    rank[j] = __popc(grp & lt) + base;
+    run_lo += c_lo;
+    run_hi += c_hi;
+  }
+  return (unsigned long long)run_lo | ((unsigned long long)run_hi << 32);
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(R1B, SH_R1_MINB) k_round1(Workspace ws) {
   constexpr int K = DIM;
@@ -216,23 +269,7 @@ __global__ void __launch_bounds__(R1B, SH_R1_MINB) k_round1(Workspace ws) {
     // per-child counts of the chunk (8 bits each, packed) and every
     // survivor's rank among its child's survivors in the chunk
     uint32_t rank[R1ITEMS];
-    unsigned long long packed = 0ull;
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int j = 0; j < R1ITEMS; j++) {
-      uint32_t r = 0;
-      unsigned long long add = 0ull;
-#pragma unroll
-      for (int k = 0; k < NK; k++) {
-        const bool mine = key[j] == (uint32_t)k;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
-        r += mine ? (uint32_t)__popc(m & lt) : 0u;
-        add += (unsigned long long)__popc(m) << (8 * k);
-      }
-      const uint32_t kj = key[j] < (uint32_t)NK ? key[j] : 0u;
-      rank[j] = r + (uint32_t)((packed >> (8 * kj)) & 0xFFull);
-      packed += add;
-    }
+    const unsigned long long packed = chunk_ranks<NK, R1ITEMS>(key, rank);
     // staged start of each child: exclusive prefix of the packed counts
     unsigned long long off = 0ull;
 #pragma unroll
@@ -592,23 +629,7 @@ __global__ void __launch_bounds__(R1B, SH_R1_MINB) k_round_long(Workspace ws) {
       hl[j] = (uint32_t)__double2loint(dn);
     }
     uint32_t rank[R1ITEMS];
-    unsigned long long packed = 0ull;
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int j = 0; j < R1ITEMS; j++) {
-      uint32_t r = 0;
-      unsigned long long add = 0ull;
-#pragma unroll
-      for (int k = 0; k < NK; k++) {
-        const bool mine = key[j] == (uint32_t)k;
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
-        r += mine ? (uint32_t)__popc(m & lt) : 0u;
-        add += (unsigned long long)__popc(m) << (8 * k);
-      }
-      const uint32_t kj = key[j] < (uint32_t)NK ? key[j] : 0u;
-      rank[j] = r + (uint32_t)((packed >> (8 * kj)) & 0xFFull);
-      packed += add;
-    }
+    const unsigned long long packed = chunk_ranks<NK, R1ITEMS>(key, rank);
     unsigned long long off = 0ull;
 #pragma unroll
     for (int k = 1; k < NK; k++)
