@@ -349,6 +349,7 @@ __device__ uint32_t wrap_query(Wrap& W, const KTree& T, const FilterParams& P, u
   }
   int top = 1;
   stk[0] = ((P.nlev - 1) << 26) | 0u;
+  __syncwarp();
   while (top > 0) {
     top--;
     const uint32_t e = stk[top];

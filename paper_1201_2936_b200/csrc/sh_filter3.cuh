@@ -617,6 +617,7 @@ __device__ Sup support_query(const FilterWs& f, const FilterParams& P, V3 d, V3 
       cl = e >> 26;
       cn = e & ((1u << 26) - 1);
       cb = stk.bound[top];
+      __syncwarp();  // every lane has read the entry before any lane pushes over it
     }
     have = false;
     if (first_hit ? !(cb > thr) : (cb < best.val)) continue;
