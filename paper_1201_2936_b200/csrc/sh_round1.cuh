@@ -74,6 +74,12 @@ __device__ __forceinline__ int classify3_bf(const Seg3& g, double qx, double qy,
 #ifndef SH_R1_MINB
 #define SH_R1_MINB 2
 #endif
+#ifndef SH_R1_MINB3
+#define SH_R1_MINB3 2
+#endif
+#ifndef SH_RL_MINB3
+#define SH_RL_MINB3 1  // 3D long rounds: no spills at one block per SM (measured faster)
+#endif
 // Ranks of a warp chunk's survivors per child (key < NK; NK <= 8): rank[j]
 // = number of earlier survivors of the same child in the chunk (item-major,
 // then lane).  Returns the chunk's per-child counts packed 8 bits each
@@ -128,7 +134,7 @@ __device__ __forceinline__ unsigned long long chunk_ranks(const uint32_t* key, u
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(R1B, SH_R1_MINB) k_round1(Workspace ws) {
+__global__ void __launch_bounds__(R1B, DIM == 2 ? SH_R1_MINB : SH_R1_MINB3) k_round1(Workspace ws) {
   constexpr int K = DIM;
   constexpr int NK = 2 * K;  // children: (side segment w, state s) -> w * K + s
   using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
@@ -387,7 +393,7 @@ __device__ __forceinline__ bool long_round(const RoundParams& rp, const DevState
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(R1B, SH_R1_MINB) k_round_long(Workspace ws) {
+__global__ void __launch_bounds__(R1B, DIM == 2 ? SH_R1_MINB : SH_RL_MINB3) k_round_long(Workspace ws) {
   constexpr int K = DIM;
   constexpr int NK = 2 * K;  // children of the window: (segment w + k / K, state k % K)
   using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
