@@ -141,4 +141,16 @@ SH_HD double from_ordered_bits(uint64_t k) {
 #endif
 }
 
+// fl(Db / nb) > fl(Da / na) (nb, na > 0): the reference compares the
+// rounded quotients (classify_three_faces, geometry.py:192-208).  When the
+// cross products Db*na and Da*nb differ by more than 1e-14 of their size the
+// exact quotients differ by far more than a rounding step, so the rounded
+// ones compare the same way and no division is needed; otherwise divide.
+SH_HD bool quotient_gt(double Db, double nb, double Da, double na) {
+  const double p = mul(Db, na), r = mul(Da, nb);
+  const double diff = sub(p, r);
+  if (fabs(diff) > mul(1e-14, add(fabs(p), fabs(r)))) return diff > 0.0;
+  return div_(Db, nb) > div_(Da, na);
+}
+
 }  // namespace sh

@@ -131,11 +131,10 @@ __device__ __forceinline__ int classify3(const Seg3& g, double qx, double qy, do
   bool inside = (D0 <= g.thr[0]) & (D1 <= g.thr[1]) & (D2 <= g.thr[2]);
   if (inside) return -1;
   // first argmax of D_j / |N_j| (np.argmax over the stacked quotients)
-  double q0 = div_(D0, g.nrm[0]), q1 = div_(D1, g.nrm[1]), q2 = div_(D2, g.nrm[2]);
   int state = 0;
-  double qb = q0, db = D0;
-  if (q1 > qb) { state = 1; qb = q1; db = D1; }
-  if (q2 > qb) { state = 2; db = D2; }
+  double db = D0, nb = g.nrm[0];
+  if (quotient_gt(D1, g.nrm[1], db, nb)) { state = 1; db = D1; nb = g.nrm[1]; }
+  if (quotient_gt(D2, g.nrm[2], db, nb)) { state = 2; db = D2; }
   *dnext = db;
   return state;
 }

@@ -55,15 +55,15 @@ __device__ __forceinline__ int classify3_bf(const Seg3& g, double qx, double qy,
   const double D1 = plane_dist(g.N[1], g.b, qx, qy, qz);
   const double D2 = plane_dist(g.N[2], g.c, qx, qy, qz);
   const bool inside = (D0 <= g.thr[0]) & (D1 <= g.thr[1]) & (D2 <= g.thr[2]);
-  const double q0 = div_(D0, g.nrm[0]), q1 = div_(D1, g.nrm[1]), q2 = div_(D2, g.nrm[2]);
+  // first argmax of the rounded quotients D_j / |N_j| (quotient_gt)
   int state = 0;
-  double qb = q0, db = D0;
-  if (q1 > qb) {
+  double db = D0, nb = g.nrm[0];
+  if (quotient_gt(D1, g.nrm[1], db, nb)) {
     state = 1;
-    qb = q1;
     db = D1;
+    nb = g.nrm[1];
   }
-  if (q2 > qb) {
+  if (quotient_gt(D2, g.nrm[2], db, nb)) {
     state = 2;
     db = D2;
   }
