@@ -59,7 +59,7 @@ struct FilterParams {
   double lo[3], inv_h[3], ctr[3];
   double gsum[3];              // sum of the candidates (deterministic order)
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
-  uint32_t ambiguous, gjk_capped, pad0, pad1;
+  uint32_t ambiguous, gjk_capped, nwl, ctr_wl;  // nwl: work-list length (k_f_cert)
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
   unsigned long long local_in, local_out, fallback;
   unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;  // SM cycles per phase (summed over warps)
@@ -78,6 +78,9 @@ struct FilterWs {
   double* nbox;                      // [node][6]: lo x,y,z, hi x,y,z (all levels)
   double* nvol;                      // [node][9]: oriented slab of levels 0-1 (see k_f_vols)
   uint8_t* keep;
+  // candidates the first (certificate) query does not settle, for k_f_test
+  uint32_t *wl_ps, *wl_pos, *wl_id;
+  double* wl_val;
 };
 
 static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
@@ -97,6 +100,10 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
   A((void**)&f.sid, mcap * 4);
   A((void**)&f.spos, mcap * 4);
   A((void**)&f.keep, mcap);
+  A((void**)&f.wl_ps, mcap * 4);
+  A((void**)&f.wl_pos, mcap * 4);
+  A((void**)&f.wl_id, mcap * 4);
+  A((void**)&f.wl_val, mcap * 8);
   A((void**)&f.cell_cnt, cells * 4);
   A((void**)&f.cell_start, (cells + 1) * 4);
   A((void**)&f.cell_cur, cells * 4);
@@ -108,7 +115,8 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
 
 static inline void filter_free(FilterWs& f) {
   void* ps[] = {f.result, f.fp, f.cx, f.cy, f.cz, f.sx, f.sy, f.sz, f.ccell, f.sid, f.spos, f.keep,
-                f.cell_cnt, f.cell_start, f.cell_cur, f.nbox, f.nvol};
+                f.cell_cnt, f.cell_start, f.cell_cur, f.nbox, f.nvol,
+                f.wl_ps, f.wl_pos, f.wl_id, f.wl_val};
   for (void* p : ps)
     if (p) cudaFree(p);
   f = FilterWs{};
@@ -163,6 +171,8 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
     P->ctr_test = 0;
     P->ambiguous = 0;
     P->gjk_capped = 0;
+    P->nwl = 0;
+    P->ctr_wl = 0;
     P->queries = 0;
     P->scanned = 0;
     P->gjk_iters = 0;
@@ -893,28 +903,26 @@ constexpr int F_EXTRA = SH_F_EXTRA;  // global points added to the local set  //
 
 // 1 keep, 0 prune; *amb set when kept only because v is within eps of the
 // boundary of the other candidates' hull (or the iteration cap was hit).
-__device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, uint32_t i, V3 v, V3 ctr,
-                        V3 gsum, double eps, int* amb, int* capped, FStack& stk, FStat& fs) {
-  const int lane = threadIdx.x & 31;
+// direction of the certificate query: v - centre of the candidates' box
+__device__ __forceinline__ V3 f_cert_dir(V3 v, V3 ctr, double* len) {
   V3 w0 = vsub(v, ctr);
   double wl = sqrt_(vdot(w0, w0));
   if (!(wl > 0.0)) {
     w0 = v3(1.0, 0.0, 0.0);
     wl = 1.0;
   }
-  // (0) certificate along v - centre (one existence query)
-  const double thr0 = mul(eps, wl);
+  *len = wl;
+  return w0;
+}
+
+// (1)-(3) for a candidate whose certificate query (k_f_cert) found the
+// candidate s0 above v's radial plane
+__device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, uint32_t i, V3 v, V3 ctr,
+                        V3 gsum, double eps, Sup s0, int* amb, int* capped, FStack& stk, FStat& fs) {
+  const int lane = threadIdx.x & 31;
+  double wl;
+  const V3 w0 = f_cert_dir(v, ctr, &wl);
   long long tc = FCLK();
-  const Sup s0 = support_query(f, P, w0, v, i, thr0, true, stk, fs);
-  {
-    const long long t2 = FCLK();
-    fs.cyc_cert += (unsigned long long)(t2 - tc);
-    tc = t2;
-  }
-  if (!(s0.val > thr0)) {
-    fs.certified++;
-    return 1;
-  }
   int iters = 0;
   // (1) local GJK: the candidate's Morton neighbours plus the centroid of
   // all other candidates (a convex combination of them, so any simplex it
@@ -1074,10 +1082,10 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   return 1;
 }
 
-#ifndef SH_FTEST_MINB
-#define SH_FTEST_MINB 3
-#endif
-__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspace ws, FilterWs f) {
+// (0) certificate queries, one warp per candidate (Morton order): a light
+// kernel (the support query only) at high occupancy; the candidates it
+// does not settle go to a work list for k_f_test
+__global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_cert(Workspace ws, FilterWs f) {
   __shared__ FilterParams sP;
   __shared__ FStack s_stk[F_TEST_BLOCK / 32];
   if (threadIdx.x == 0) sP = *f.fp;
@@ -1086,22 +1094,79 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
   const uint32_t m = P.m;
   const double eps = ws.st->eps;
   const V3 ctr = v3(P.ctr[0], P.ctr[1], P.ctr[2]);
+  const int lane = threadIdx.x & 31;
+  FStack& stk = s_stk[threadIdx.x >> 5];
+  FStat fs = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (;;) {
+    uint32_t ps = 0;
+    if (lane == 0) ps = atomicAdd(&f.fp->ctr_test, 1u);
+    ps = __shfl_sync(0xFFFFFFFFu, ps, 0);
+    if (ps >= m) break;
+    const uint32_t i = __ldg(&f.sid[ps]);
+    if (m <= 4) {  // quickhull.py:148-149
+      if (lane == 0) f.keep[i] = 1;
+      continue;
+    }
+    const V3 v = v3(f.cx[i], f.cy[i], f.cz[i]);
+    double wl;
+    const V3 w0 = f_cert_dir(v, ctr, &wl);
+    const double thr0 = mul(eps, wl);
+    const long long tc = FCLK();
+    const Sup s0 = support_query(f, P, w0, v, i, thr0, true, stk, fs);
+    fs.cyc_cert += (unsigned long long)(FCLK() - tc);
+    if (lane == 0) {
+      if (!(s0.val > thr0)) {
+        f.keep[i] = 1;
+        fs.certified++;
+      } else {
+        const uint32_t k = atomicAdd(&f.fp->nwl, 1u);
+        f.wl_ps[k] = ps;
+        f.wl_pos[k] = s0.pos;
+        f.wl_id[k] = s0.id;
+        f.wl_val[k] = s0.val;
+      }
+    }
+  }
+  if (lane == 0 && fs.queries) {
+    atomicAdd(&f.fp->queries, fs.queries);
+    atomicAdd(&f.fp->scanned, fs.scanned);
+    atomicAdd(&f.fp->certified, fs.certified);
+    atomicAdd(&f.fp->cyc_cert, fs.cyc_cert);
+  }
+}
+
+#ifndef SH_FTEST_MINB
+#define SH_FTEST_MINB 3
+#endif
+// (1)-(3) for the work list of k_f_cert
+__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspace ws, FilterWs f) {
+  __shared__ FilterParams sP;
+  __shared__ FStack s_stk[F_TEST_BLOCK / 32];
+  if (threadIdx.x == 0) sP = *f.fp;
+  __syncthreads();
+  const FilterParams& P = sP;
+  const uint32_t nwl = P.nwl;
+  const double eps = ws.st->eps;
+  const V3 ctr = v3(P.ctr[0], P.ctr[1], P.ctr[2]);
   const V3 gsum = v3(P.gsum[0], P.gsum[1], P.gsum[2]);
   const int lane = threadIdx.x & 31;
   FStack& stk = s_stk[threadIdx.x >> 5];
   int amb_count = 0, cap_count = 0;
   FStat fs = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (;;) {
-    // candidates in Morton order: warps of a block work on nearby candidates
-    // and share the tree nodes they touch in L1
-    uint32_t ps = 0;
-    if (lane == 0) ps = atomicAdd(&f.fp->ctr_test, 1u);
-    ps = __shfl_sync(0xFFFFFFFFu, ps, 0);
-    if (ps >= m) break;
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(&f.fp->ctr_wl, 1u);
+    k = __shfl_sync(0xFFFFFFFFu, k, 0);
+    if (k >= nwl) break;
+    const uint32_t ps = f.wl_ps[k];
     const uint32_t i = __ldg(&f.sid[ps]);
-    int keep = 1, amb = 0, capped = 0;
-    if (m > 4)
-      keep = f_decide(f, P, ps, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, gsum, eps, &amb, &capped, stk, fs);
+    Sup s0;
+    s0.pos = f.wl_pos[k];
+    s0.id = f.wl_id[k];
+    s0.val = f.wl_val[k];
+    int amb = 0, capped = 0;
+    const int keep = f_decide(f, P, ps, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, gsum, eps, s0, &amb, &capped,
+                              stk, fs);
     if (lane == 0) {
       f.keep[i] = (uint8_t)keep;
       amb_count += amb;
@@ -1114,11 +1179,9 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
     atomicAdd(&f.fp->queries, fs.queries);
     atomicAdd(&f.fp->scanned, fs.scanned);
     atomicAdd(&f.fp->gjk_iters, fs.iters);
-    atomicAdd(&f.fp->certified, fs.certified);
     atomicAdd(&f.fp->local_in, fs.local_in);
     atomicAdd(&f.fp->local_out, fs.local_out);
     atomicAdd(&f.fp->fallback, fs.fallback);
-    atomicAdd(&f.fp->cyc_cert, fs.cyc_cert);
     atomicAdd(&f.fp->cyc_local, fs.cyc_local);
     atomicAdd(&f.fp->cyc_out, fs.cyc_out);
     atomicAdd(&f.fp->cyc_fallback, fs.cyc_fallback);
@@ -1174,6 +1237,7 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(f);
   k_f_boxes_hi<<<1, 1024, 0, s>>>(f);
   k_f_vols<<<nsm * 4, BLOCK, 0, s>>>(f);
+  k_f_cert<<<nsm * 16, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_test<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_compact<<<1, 1024, 0, s>>>(ws, f);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 10;
