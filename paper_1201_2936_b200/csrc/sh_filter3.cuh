@@ -1085,7 +1085,10 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
 // (0) certificate queries, one warp per candidate (Morton order): a light
 // kernel (the support query only) at high occupancy; the candidates it
 // does not settle go to a work list for k_f_test
-__global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_cert(Workspace ws, FilterWs f) {
+#ifndef SH_FCERT_MINB
+#define SH_FCERT_MINB 8
+#endif
+__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FCERT_MINB) k_f_cert(Workspace ws, FilterWs f) {
   __shared__ FilterParams sP;
   __shared__ FStack s_stk[F_TEST_BLOCK / 32];
   if (threadIdx.x == 0) sP = *f.fp;
@@ -1136,7 +1139,7 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, 8) k_f_cert(Workspace ws, Filter
 }
 
 #ifndef SH_FTEST_MINB
-#define SH_FTEST_MINB 3
+#define SH_FTEST_MINB 2
 #endif
 // (1)-(3) for the work list of k_f_cert
 __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspace ws, FilterWs f) {
