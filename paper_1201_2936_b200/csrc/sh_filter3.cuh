@@ -60,6 +60,7 @@ struct FilterParams {
   double gsum[3];              // sum of the candidates (deterministic order)
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
   uint32_t ambiguous, gjk_capped, nwl, ctr_wl;  // nwl: work-list length (k_f_cert)
+  uint32_t nwl2, ctr_wl2, pad2, pad3;            // second work list (k_f_local)
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
   unsigned long long local_in, local_out, fallback;
   unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;  // SM cycles per phase (summed over warps)
@@ -81,6 +82,11 @@ struct FilterWs {
   // candidates the first (certificate) query does not settle, for k_f_test
   uint32_t *wl_ps, *wl_pos, *wl_id;
   double* wl_val;
+  // candidates the first local GJK (k_f_local) does not prune, for k_f_test:
+  // work-list index (| 1 << 31 when the local GJK was inconclusive) and the
+  // separating direction it found
+  uint32_t* wl2_k;
+  double* wl2_sep;
 };
 
 static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
@@ -104,6 +110,8 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
   A((void**)&f.wl_pos, mcap * 4);
   A((void**)&f.wl_id, mcap * 4);
   A((void**)&f.wl_val, mcap * 8);
+  A((void**)&f.wl2_k, mcap * 4);
+  A((void**)&f.wl2_sep, mcap * 24);
   A((void**)&f.cell_cnt, cells * 4);
   A((void**)&f.cell_start, (cells + 1) * 4);
   A((void**)&f.cell_cur, cells * 4);
@@ -116,7 +124,7 @@ static inline int filter_alloc(FilterWs& f, uint64_t mcap) {
 static inline void filter_free(FilterWs& f) {
   void* ps[] = {f.result, f.fp, f.cx, f.cy, f.cz, f.sx, f.sy, f.sz, f.ccell, f.sid, f.spos, f.keep,
                 f.cell_cnt, f.cell_start, f.cell_cur, f.nbox, f.nvol,
-                f.wl_ps, f.wl_pos, f.wl_id, f.wl_val};
+                f.wl_ps, f.wl_pos, f.wl_id, f.wl_val, f.wl2_k, f.wl2_sep};
   for (void* p : ps)
     if (p) cudaFree(p);
   f = FilterWs{};
@@ -173,6 +181,8 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
     P->gjk_capped = 0;
     P->nwl = 0;
     P->ctr_wl = 0;
+    P->nwl2 = 0;
+    P->ctr_wl2 = 0;
     P->queries = 0;
     P->scanned = 0;
     P->gjk_iters = 0;
@@ -917,8 +927,14 @@ __device__ __forceinline__ V3 f_cert_dir(V3 v, V3 ctr, double* len) {
 
 // (1)-(3) for a candidate whose certificate query (k_f_cert) found the
 // candidate s0 above v's radial plane
+// mode 0: everything; mode 1: the first local GJK (k_f_local) already
+// separated v from the local set along sep_in; mode 2: it was inconclusive,
+// go straight to the global GJK; mode 3: the first local GJK only (returns
+// 0 = pruned, 1 = separated along *sep_out, 2 = inconclusive)
+template <int MODE>
 __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, uint32_t i, V3 v, V3 ctr,
-                        V3 gsum, double eps, Sup s0, int* amb, int* capped, FStack& stk, FStat& fs) {
+                        V3 gsum, double eps, Sup s0, int* amb, int* capped, FStack& stk, FStat& fs,
+                        V3 sep_in = V3{0.0, 0.0, 0.0}, V3* sep_out = nullptr) {
   const int lane = threadIdx.x & 31;
   double wl;
   const V3 w0 = f_cert_dir(v, ctr, &wl);
@@ -927,7 +943,7 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   // (1) local GJK: the candidate's Morton neighbours plus the centroid of
   // all other candidates (a convex combination of them, so any simplex it
   // spans with candidates lies in their hull)
-  {
+  if (MODE != 2) {
     const uint32_t lo = ps > 16u * F_LOCAL ? ps - 16u * F_LOCAL : 0u;
     V3 lu[F_LOCAL];
     uint32_t lid[F_LOCAL];
@@ -1013,8 +1029,19 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
 #pragma unroll 1
     for (int xr = 0; xr <= F_EXTRA; xr++) {
       iters = 0;
-      const int r = gjk(local_sup, first, eps, &sep, &iters);
+      int r;
+      if (MODE == 1 && xr == 0) {
+        r = GJK_OUTSIDE;
+        sep = sep_in;
+      } else {
+        r = gjk(local_sup, first, eps, &sep, &iters);
+      }
       fs.iters += iters;
+      if (MODE == 3) {
+        if (r == GJK_INSIDE) fs.local_in++;
+        *sep_out = sep;
+        return r == GJK_INSIDE ? 0 : (r == GJK_OUTSIDE ? 1 : 2);
+      }
       {
         const long long t2 = FCLK();
         fs.cyc_local += (unsigned long long)(t2 - tc);
@@ -1049,6 +1076,7 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
       first.u = cu;
     }
   }
+  if (MODE == 3) return 2;
   fs.fallback++;
   struct CycGuard {
     FStat& s;
@@ -1141,8 +1169,9 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FCERT_MINB) k_f_cert(Workspac
 #ifndef SH_FTEST_MINB
 #define SH_FTEST_MINB 2
 #endif
-// (1)-(3) for the work list of k_f_cert
-__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspace ws, FilterWs f) {
+// the first local GJK for the work list of k_f_cert: pruned candidates are
+// settled here, the rest go to a second work list with the outcome
+__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_local(Workspace ws, FilterWs f) {
   __shared__ FilterParams sP;
   __shared__ FStack s_stk[F_TEST_BLOCK / 32];
   if (threadIdx.x == 0) sP = *f.fp;
@@ -1154,7 +1183,6 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
   const V3 gsum = v3(P.gsum[0], P.gsum[1], P.gsum[2]);
   const int lane = threadIdx.x & 31;
   FStack& stk = s_stk[threadIdx.x >> 5];
-  int amb_count = 0, cap_count = 0;
   FStat fs = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (;;) {
     uint32_t k = 0;
@@ -1168,8 +1196,63 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
     s0.id = f.wl_id[k];
     s0.val = f.wl_val[k];
     int amb = 0, capped = 0;
-    const int keep = f_decide(f, P, ps, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, gsum, eps, s0, &amb, &capped,
-                              stk, fs);
+    V3 sep;
+    const int r = f_decide<3>(f, P, ps, i, v3(f.cx[i], f.cy[i], f.cz[i]), ctr, gsum, eps, s0, &amb, &capped,
+                              stk, fs, V3{0.0, 0.0, 0.0}, &sep);
+    if (lane == 0) {
+      if (r == 0) {
+        f.keep[i] = 0;
+      } else {
+        const uint32_t j = atomicAdd(&f.fp->nwl2, 1u);
+        f.wl2_k[j] = k | (r == 2 ? 0x80000000u : 0u);
+        f.wl2_sep[3 * j + 0] = sep.x;
+        f.wl2_sep[3 * j + 1] = sep.y;
+        f.wl2_sep[3 * j + 2] = sep.z;
+      }
+    }
+  }
+  if (lane == 0 && fs.iters) {
+    atomicAdd(&f.fp->gjk_iters, fs.iters);
+    atomicAdd(&f.fp->local_in, fs.local_in);
+  }
+}
+
+// (2)-(3) for the candidates the first local GJK separated or could not decide
+__global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspace ws, FilterWs f) {
+  __shared__ FilterParams sP;
+  __shared__ FStack s_stk[F_TEST_BLOCK / 32];
+  if (threadIdx.x == 0) sP = *f.fp;
+  __syncthreads();
+  const FilterParams& P = sP;
+  const uint32_t nwl2 = P.nwl2;
+  const double eps = ws.st->eps;
+  const V3 ctr = v3(P.ctr[0], P.ctr[1], P.ctr[2]);
+  const V3 gsum = v3(P.gsum[0], P.gsum[1], P.gsum[2]);
+  const int lane = threadIdx.x & 31;
+  FStack& stk = s_stk[threadIdx.x >> 5];
+  int amb_count = 0, cap_count = 0;
+  FStat fs = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (;;) {
+    uint32_t j = 0;
+    if (lane == 0) j = atomicAdd(&f.fp->ctr_wl2, 1u);
+    j = __shfl_sync(0xFFFFFFFFu, j, 0);
+    if (j >= nwl2) break;
+    const uint32_t kk = f.wl2_k[j];
+    const uint32_t k = kk & 0x7FFFFFFFu;
+    const uint32_t ps = f.wl_ps[k];
+    const uint32_t i = __ldg(&f.sid[ps]);
+    Sup s0;
+    s0.pos = f.wl_pos[k];
+    s0.id = f.wl_id[k];
+    s0.val = f.wl_val[k];
+    const V3 v = v3(f.cx[i], f.cy[i], f.cz[i]);
+    int amb = 0, capped = 0, keep;
+    if (kk & 0x80000000u) {
+      keep = f_decide<2>(f, P, ps, i, v, ctr, gsum, eps, s0, &amb, &capped, stk, fs);
+    } else {
+      const V3 sep = v3(f.wl2_sep[3 * j + 0], f.wl2_sep[3 * j + 1], f.wl2_sep[3 * j + 2]);
+      keep = f_decide<1>(f, P, ps, i, v, ctr, gsum, eps, s0, &amb, &capped, stk, fs, sep);
+    }
     if (lane == 0) {
       f.keep[i] = (uint8_t)keep;
       amb_count += amb;
@@ -1241,6 +1324,7 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_boxes_hi<<<1, 1024, 0, s>>>(f);
   k_f_vols<<<nsm * 4, BLOCK, 0, s>>>(f);
   k_f_cert<<<nsm * 16, F_TEST_BLOCK, 0, s>>>(ws, f);
+  k_f_local<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_test<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_compact<<<1, 1024, 0, s>>>(ws, f);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 10;
