@@ -143,6 +143,69 @@ def gen(kind, n, start=0):
     return generate(kind, n, 0, start=start)
 
 
+def measure_roofline(L, ctx, device, launch, n, dim, config, hull_ms):
+    """roofline object of the round kernels: per-launch CUDA events (launch
+    mode 2) around one hull run by ``launch()`` on ``ctx``; bytes per launch
+    from the per-round trace."""
+    import paper_1201_2936_b200 as P
+    L.sh_set_launch_mode(ctx, 2)
+    per = []
+    for _ in range(3):
+        launch()
+        import torch
+        torch.cuda.synchronize()
+        kinds = np.zeros(4096, np.int32)
+        ms = np.zeros(4096, np.float32)
+        k = L.sh_launch_times(ctx, kinds.ctypes.data, ms.ctypes.data, 4096)
+        per.append((kinds[:k].copy(), ms[:k].copy()))
+    L.sh_set_launch_mode(ctx, 0)
+    tr = P.trace(device)  # of the hull just measured
+    Rd = 8 * dim + 4
+    n1 = int(tr[0, 0]) if len(tr) else 0
+    # bytes each round launch must move in this design: the first split
+    # reads the input and writes nothing; round 1 re-reads the input (the
+    # split is re-derived on the fly) and writes its survivors; later rounds
+    # read and write R_d-byte records
+    round_bytes = [8 * dim * n]
+    for r, (a, b, _, _) in enumerate(tr):
+        round_bytes.append((8 * dim * n if r == 0 else Rd * int(a)) + Rd * int(b))
+    # SURVEY.md §8(d)'s canonical B_alg (materialised first split)
+    b_alg = 2 * 8 * dim * n + Rd * n1 + sum(Rd * (int(a) + int(b)) for a, b, _, _ in tr)
+    best = None
+    kernel_ms_by_kind = {}
+    for kinds, ms in per:
+        rt = ms[(kinds == KID_ROUND_FIRST) | (kinds == KID_ROUND)]
+        if len(rt) != len(round_bytes):
+            continue
+        tot_round = float(rt.sum())
+        if best is None or tot_round < best[0]:
+            best = (tot_round, float(ms.sum()), rt)
+            names = ["init", "first_reduce", "line_far", "round_first", "round", "book", "filter",
+                     "output", "facets"]
+            kernel_ms_by_kind = {names[k]: round(float(ms[kinds == k].sum()), 4)
+                                 for k in sorted(set(kinds.tolist()))}
+    if not best:
+        return None
+    peak, peak_src = measured_peak()
+    tot_round, tot_all, rt = best
+    launches = len(round_bytes)
+    achieved = sum(round_bytes) / launches / (tot_round / launches / 1e3) / 1e9
+    return {"bound": "hbm",
+            "kernel": "k_round1 (round 1, fused with the first split) + k_round (rounds >= 2): "
+                      "discard+classify+regroup+argmax",
+            "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": committed_traffic(config),
+            "peak_source": peak_src, "launches": launches,
+            "algorithmic_bytes_per_launch": int(sum(round_bytes) / launches),
+            "avg_launch_ms": round(tot_round / launches, 4),
+            "share_of_kernel_time": round(tot_round / tot_all, 3),
+            "whole_hull_frac": round(b_alg / (hull_ms / 1e3) / 1e9 / peak, 4),
+            "whole_hull_b_alg_bytes": b_alg,
+            "design_bytes_per_hull": sum(round_bytes) + 8 * dim * n,
+            "per_round_gbs": [round(float(b / (t / 1e3) / 1e9), 1) for b, t in zip(round_bytes, rt)],
+            "kernel_ms_by_kind": kernel_ms_by_kind}
+
+
 def run_sharded(args, ws, rank, local):
     """N GPUs, weak scaling: rank r hulls points [r*n, (r+1)*n) of one N*n
     cloud of the configured kind; the global hull is assembled by
@@ -201,6 +264,23 @@ def run_sharded(args, ws, rank, local):
         if i:
             e2e_ms.append(float(t.item()))
     e2e_val = n * ws / (statistics.mean(e2e_ms) / 1e3) / 1e6
+    # round-kernel roofline of this rank's local hull (same kernels as N=1,
+    # with the global eps), measured on rank 0
+    roofline = None
+    if rank == 0:
+        from paper_1201_2936_b200 import _lib
+        import paper_1201_2936_b200 as P
+        L, ctx = _lib.lib(), _lib.context(local)
+        f = P.hull_indices_2d if dim == 2 else P.hull_indices_3d
+        tol = P.Tolerance(eps_abs=info["eps"])
+        roofline = measure_roofline(L, ctx, local, lambda: f(d, tol), n, dim, args.config,
+                                    tot_ms / args.steps)
+    launches = None
+    if roofline:
+        # per rank and step: bbox (3 kernels) + the local hull (as in main());
+        # rank 0's merge hull of the gathered candidates is not counted
+        r = roofline["launches"] - 1
+        launches = args.steps * (3 + 5 + 2 * r + min(3, max(0, r - 1)) + (11 if dim == 3 else 0))
     if rank == 0:
         h = int(res.numel())
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
@@ -216,7 +296,7 @@ def run_sharded(args, ws, rank, local):
                 "e2e": {"value": round(e2e_val, 2), "unit": UNIT,
                         "h2d_bytes_per_step": 8 * dim * n * ws, "d2h_bytes_per_step": 8 * h,
                         "ms_per_step": round(statistics.mean(e2e_ms), 3)},
-                "gpu_launches": None, "roofline": None, "cpu_baseline": None, "clocks": clocks}
+                "gpu_launches": launches, "roofline": roofline, "cpu_baseline": None, "clocks": clocks}
         print(json.dumps(line), flush=True)
 
 
@@ -280,6 +360,9 @@ def main():
 
     torch.cuda.set_device(local)
     if ws > 1 or args.sharded:
+        # NCCL's version banner goes to stdout, where rank 0 must print one
+        # JSON line only
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
@@ -365,59 +448,7 @@ def main():
     launches_per_hull = 5 + 2 * rounds + peeled + (10 if dim == 3 else 0) + (8 if want_fac else 0)
 
     # ---------------- per-kernel pass (events after every launch)
-    tr = P.trace(local)
-    L.sh_set_launch_mode(ctx, 2)
-    per = []
-    for _ in range(3):
-        launch()
-        torch.cuda.synchronize()
-        kinds = np.zeros(4096, np.int32)
-        ms = np.zeros(4096, np.float32)
-        k = L.sh_launch_times(ctx, kinds.ctypes.data, ms.ctypes.data, 4096)
-        per.append((kinds[:k].copy(), ms[:k].copy()))
-    L.sh_set_launch_mode(ctx, 0)
-    Rd = 8 * dim + 4
-    n1 = int(tr[0, 0]) if len(tr) else 0
-    # bytes each k_round launch must move in this design: the first split
-    # reads the input and writes nothing; round 1 re-reads the input (the
-    # split is re-derived on the fly) and writes its survivors; later rounds
-    # read and write R_d-byte records
-    round_bytes = [8 * dim * n]
-    for r, (a, b, _, _) in enumerate(tr):
-        round_bytes.append((8 * dim * n if r == 0 else Rd * int(a)) + Rd * int(b))
-    # SURVEY.md §8(d)'s canonical B_alg (materialised first split)
-    b_alg = 2 * 8 * dim * n + Rd * n1 + sum(Rd * (int(a) + int(b)) for a, b, _, _ in tr)
-    best = None
-    for kinds, ms in per:
-        rt = ms[(kinds == KID_ROUND_FIRST) | (kinds == KID_ROUND)]
-        if len(rt) != len(round_bytes):
-            continue
-        tot_round = float(rt.sum())
-        if best is None or tot_round < best[0]:
-            best = (tot_round, float(ms.sum()), rt)
-            names = ["init", "first_reduce", "line_far", "round_first", "round", "book", "filter",
-                     "output", "facets"]
-            kernel_ms_by_kind = {names[k]: round(float(ms[kinds == k].sum()), 4)
-                                 for k in sorted(set(kinds.tolist()))}
-    peak, peak_src = measured_peak()
-    roofline = None
-    if best:
-        tot_round, tot_all, rt = best
-        launches = len(round_bytes)
-        achieved = sum(round_bytes) / launches / (tot_round / launches / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_round1 (round 1, fused with the first split) + k_round (rounds >= 2): discard+classify+regroup+argmax",
-                    "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": committed_traffic(args.config),
-                    "peak_source": peak_src, "launches": launches,
-                    "algorithmic_bytes_per_launch": int(sum(round_bytes) / launches),
-                    "avg_launch_ms": round(tot_round / launches, 4),
-                    "share_of_kernel_time": round(tot_round / tot_all, 3),
-                    "whole_hull_frac": round(b_alg / (tot_ms / args.steps / 1e3) / 1e9 / peak, 4),
-                    "whole_hull_b_alg_bytes": b_alg,
-                    "design_bytes_per_hull": sum(round_bytes) + 8 * dim * n,
-                    "per_round_gbs": [round(float(b / (t / 1e3) / 1e9), 1) for b, t in
-                                      zip(round_bytes, rt)],
-                    "kernel_ms_by_kind": kernel_ms_by_kind}
+    roofline = measure_roofline(L, ctx, local, launch, n, dim, args.config, tot_ms / args.steps)
 
     # ---------------- e2e: public API, pinned host buffers in, indices out
     e2e_ms = []
