@@ -280,7 +280,7 @@ def run_sharded(args, ws, rank, local):
         # per rank and step: bbox (3 kernels) + the local hull (as in main());
         # rank 0's merge hull of the gathered candidates is not counted
         r = roofline["launches"] - 1
-        launches = args.steps * (3 + 5 + 2 * r + min(3, max(0, r - 1)) + (13 if dim == 3 else 0))
+        launches = args.steps * (3 + 5 + 2 * r + min(3, max(0, r - 1)) + (12 if dim == 3 else 0))
     if rank == 0:
         h = int(res.numel())
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
@@ -443,10 +443,10 @@ def main():
     # init, first reduce, first-split count, book, then (round, book) per
     # round, then output (2D) or line-far + 9 filter kernels (3D)
     # + one unused launch per peeled round (k_round_long / k_round pair,
-    # rounds 2..4 outside the WHILE node); 3D: line-far + 12 filter kernels;
-    # facets: 9 kernels
+    # rounds 2..4 outside the WHILE node); 3D: line-far + 12 filter kernels
+    # instead of k_output; facets: 9 kernels
     peeled = max(0, min(3, rounds - 1))
-    launches_per_hull = 5 + 2 * rounds + peeled + (13 if dim == 3 else 0) + (9 if want_fac else 0)
+    launches_per_hull = 5 + 2 * rounds + peeled + (12 if dim == 3 else 0) + (9 if want_fac else 0)
 
     # ---------------- per-kernel pass (events after every launch)
     roofline = measure_roofline(L, ctx, local, launch, n, dim, args.config, tot_ms / args.steps)
