@@ -105,6 +105,12 @@ int64_t sh_trace(sh_ctx* ctx, int64_t* live, int64_t* kept, int64_t* nseg, int64
 int sh_bbox(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride, int64_t n,
             int dim, double* out, void* stream);
 
+/* Device bytes the context allocates for `dim`-D hulls of n points with the
+ * default table capacities: the ping-pong record streams (2 * dim streams of
+ * (8*dim + 4)-byte records, capacity n each) plus segment tables sized for
+ * n / 8 segments (C2: 11.3 GB); -1 for bad arguments.  No GPU needed. */
+int64_t sh_workspace_bytes(int dim, int64_t n);
+
 /* Reserve workspace for `dim`-D hulls of up to n points (optional). */
 int sh_reserve(sh_ctx* ctx, int dim, int64_t n);
 

@@ -20,7 +20,7 @@ SH_FLAG_COLLINEAR = 1
 EXPORTED = ("sh_create", "sh_destroy", "sh_hull2d", "sh_hull3d", "sh_hull2d_async",
             "sh_hull3d_async", "sh_fetch", "sh_trace", "sh_reserve", "sh_hypot_host",
             "sh_set_launch_mode", "sh_launch_times", "sh_filter_stats", "sh_bbox", "sh_segmented_scan", "sh_flag_permute",
-            "sh_compact", "sh_scatter", "sh_orient_host", "sh_uniform_points", "sh_facet_stats", "sh_last_error", "sh_version")
+            "sh_compact", "sh_scatter", "sh_orient_host", "sh_workspace_bytes", "sh_uniform_points", "sh_facet_stats", "sh_last_error", "sh_version")
 
 
 class ShResult(ctypes.Structure):
@@ -94,6 +94,8 @@ def lib():
             L.sh_orient_host.restype = ctypes.c_int
             L.sh_uniform_points.argtypes = [P, ctypes.c_int, I64, ctypes.c_uint64, I64, ctypes.c_int, P, P]
             L.sh_uniform_points.restype = ctypes.c_int
+            L.sh_workspace_bytes.argtypes = [ctypes.c_int, I64]
+            L.sh_workspace_bytes.restype = I64
             L.sh_facet_stats.argtypes = [P, P, I64]
             L.sh_facet_stats.restype = ctypes.c_int
             L.sh_filter_stats.argtypes = [P, P, I64]

@@ -595,6 +595,30 @@ void sh_destroy(sh_ctx* c) {
   delete c;
 }
 
+int64_t sh_workspace_bytes(int dim, int64_t n) {
+  // mirrors alloc_ws / filter_alloc with the default capacities (the
+  // workspace only grows past them when a hull overflows, see hull_sync)
+  if ((dim != 2 && dim != 3) || n <= 0) return -1;
+  const uint64_t K = dim, rcap = (uint64_t)n + 16;
+  const uint64_t segcap = default_segcap(dim, (uint64_t)n);
+  const uint64_t max_tiles = ((uint64_t)n + RTILE - 1) / RTILE + 4;
+  (void)max_tiles;
+  const uint64_t book_tiles = (K * segcap + TILE3 - 1) / TILE3 + 4;
+  const uint64_t seg_bytes = dim == 2 ? sizeof(Seg2) : sizeof(Seg3);
+  uint64_t b = 0;
+  b += 2 * (K * rcap * (8 * K + 4));                        // ping-pong records
+  b += 2 * (segcap * seg_bytes + 4 * (segcap + 4) + 8 * (segcap + 4) + 4 * (K * segcap + 4));
+  b += sizeof(Key128) * (K * segcap + 4) + 8 * book_tiles * 4 + 4 * ((uint64_t)n + 8);
+  b += sizeof(DevState);
+  if (dim == 3) {
+    const uint64_t mcap = default_mcap((uint64_t)n);
+    const uint64_t cells = (uint64_t)FG_MAX * FG_MAX * FG_MAX;
+    const uint64_t nodes = mcap / 31 + 2 * F_LEVELS + 8;
+    b += mcap * (6 * 8 + 4 * 3 + 1 + 3 * 4 + 8 + 4 + 24) + cells * 12 + nodes * (48 + 72);
+  }
+  return (int64_t)b;
+}
+
 int sh_reserve(sh_ctx* c, int dim, int64_t n) {
   if (!c || (dim != 2 && dim != 3) || n <= 0) return set_err(SH_CONTRACT, "bad reserve arguments");
   CK(cudaSetDevice(c->device));
