@@ -745,7 +745,10 @@ __global__ void __launch_bounds__(128) k_fac_seeds(Workspace ws, FilterWs f, Fac
 }
 
 // ------------------------------------------------------------------ F7c
-__global__ void __launch_bounds__(FAC_BLOCK) k_fac_wrap(Workspace ws, FacetWs w) {
+#ifndef SH_FAC_MINB
+#define SH_FAC_MINB 4
+#endif
+__global__ void __launch_bounds__(FAC_BLOCK, SH_FAC_MINB) k_fac_wrap(Workspace ws, FacetWs w) {
   __shared__ FilterParams sP;
   __shared__ uint32_t s_stk[FAC_BLOCK / 32][F_STACK];
   if (threadIdx.x == 0) sP = *w.kfp;
