@@ -683,7 +683,9 @@ __device__ Sup support_query(const FilterWs& f, const FilterParams& P, V3 d, V3 
     double b = -INFINITY;
     if (ch < P.lnodes[chl]) {
       b = box_bound(f.nbox + (size_t)(P.loff[chl] + ch) * 6, d, v);
-      if (chl <= 1) b = fmin(b, vol_bound(f.nvol + (size_t)(P.loff[chl] + ch) * 9, d, v));
+      // the slab only where the box does not already prune the child
+      if (chl <= 1 && (first_hit ? b > thr : b >= best.val))
+        b = fmin(b, vol_bound(f.nvol + (size_t)(P.loff[chl] + ch) * 9, d, v));
     }
     const bool pass = first_hit ? (b > thr) : (b >= best.val && b > -INFINITY);
     uint32_t mask = __ballot_sync(0xFFFFFFFFu, pass);
