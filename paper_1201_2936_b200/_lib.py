@@ -11,7 +11,8 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libseghull_b200.so")
+# SH_LIB: an alternative build of the same library (tuning experiments)
+LIB_PATH = os.environ.get("SH_LIB") or os.path.join(_HERE, "libseghull_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 SH_OK, SH_CONTRACT, SH_EMPTY, SH_DEGENERATE, SH_ROUND_GUARD, SH_NOMEM, SH_CUDA = 0, 1, 2, 3, 4, 5, 10

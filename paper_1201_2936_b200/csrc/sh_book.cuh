@@ -28,7 +28,7 @@ namespace sh {
 
 struct BookShared {
   uint32_t tile;
-  uint32_t wsum[ITEMS3 * WARPS * 3];
+  uint32_t wsum[ITEMS3 * WARPS * 4];
   Sum3 agg, prefix;
   int stop[4];
 };
@@ -73,6 +73,9 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
   const Seg3* par3 = reinterpret_cast<const Seg3*>(ws.seg[in_b]);
   const uint32_t* par_start = ws.segstart[in_b];
   const uint32_t* cur_in = ws.cursor[in_b];
+  // 4-record aligned segments (spans rounded up, DEAD-padded): always for
+  // round 1 (k_stream writes it), for later rounds when k_stream may run them
+  const bool pad_next = bp.root || stream_eligible(ws, st, bp, bp.round + 1, K);
   Seg2* ch2 = reinterpret_cast<Seg2*>(ws.seg[out_b]);
   Seg3* ch3 = reinterpret_cast<Seg3*>(ws.seg[out_b]);
   uint32_t* segstart = ws.segstart[out_b];
@@ -88,7 +91,9 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
     const bool last_tile = tile == num_tiles - 1;
 
     RunVal v[ITEMS3];
-    uint32_t cval[ITEMS3][3];
+    // counters: occupied, span (records rounded up to 4: the next round's
+    // positions, DEAD-padded), emitted vertex, records (incl. DEAD claims)
+    uint32_t cval[ITEMS3][4];
     // 3D child face (needed before the scan for the flat test)
     double fa[ITEMS3][3], fb[ITEMS3][3], fc[ITEMS3][3], fn[ITEMS3][3], fnl[ITEMS3];
 #pragma unroll
@@ -137,15 +142,16 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
         emit = !(from_ordered_bits(v[j].hi) <= mul(eps, fnl[j]));
       }
       cval[j][0] = occ ? 1u : 0u;
-      cval[j][1] = v[j].cnt;
+      cval[j][1] = pad_next ? (v[j].cnt + 3u) & ~3u : v[j].cnt;
       cval[j][2] = emit ? 1u : 0u;
+      cval[j][3] = v[j].cnt;
     }
     // ---- block exclusive scan (striped order) of the three counters
-    uint32_t ex[ITEMS3][3];
+    uint32_t ex[ITEMS3][4];
 #pragma unroll
     for (int j = 0; j < ITEMS3; j++) {
 #pragma unroll
-      for (int q = 0; q < 3; q++) {
+      for (int q = 0; q < 4; q++) {
         uint32_t x = cval[j][q];
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -153,39 +159,39 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
           if (lane >= off) x += o;
         }
         ex[j][q] = x - cval[j][q];
-        if (lane == 31) sb.wsum[(j * WARPS + warp) * 3 + q] = x;
+        if (lane == 31) sb.wsum[(j * WARPS + warp) * 4 + q] = x;
       }
     }
     __syncthreads();
     if (warp == 0) {
 #pragma unroll
-      for (int q = 0; q < 3; q++) {
-        uint32_t w = sb.wsum[lane * 3 + q];
+      for (int q = 0; q < 4; q++) {
+        uint32_t w = sb.wsum[lane * 4 + q];
         uint32_t x = w;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           uint32_t o = __shfl_up_sync(0xFFFFFFFFu, x, off);
           if (lane >= off) x += o;
         }
-        sb.wsum[lane * 3 + q] = x - w;
+        sb.wsum[lane * 4 + q] = x - w;
         uint32_t tot = __shfl_sync(0xFFFFFFFFu, x, 31);
         if (lane == 0) sb.agg.v[q] = tot;
       }
     }
     __syncthreads();
     if (small) {
-      if (tid < 3) sb.prefix.v[tid] = s_carry.v[tid];
+      if (tid < 4) sb.prefix.v[tid] = s_carry.v[tid];
     } else if (tile > 0) {
-      if (tid == 0) lb_publish<3>(ws.lb_book, tile, tag16, LB_AGG, sb.agg.v);
-      lb_lookback<3>(ws.lb_book, tile, tag16, sb.prefix.v, sb.stop);
-    } else if (tid < 3) {
+      if (tid == 0) lb_publish<4>(ws.lb_book, tile, tag16, LB_AGG, sb.agg.v);
+      lb_lookback<4>(ws.lb_book, tile, tag16, sb.prefix.v, sb.stop);
+    } else if (tid < 4) {
       sb.prefix.v[tid] = 0;
     }
     __syncthreads();
     if (tid == 0) {
       Sum3 inc = s3_combine(sb.prefix, sb.agg);
       if (small) s_carry = inc;
-      else lb_publish<3>(ws.lb_book, tile, tag16, LB_INC, inc.v);
+      else lb_publish<4>(ws.lb_book, tile, tag16, LB_INC, inc.v);
     }
 
     // ---- build child tables, emit vertices
@@ -194,13 +200,21 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
       if (!cval[j][0]) continue;
       uint32_t e = base + j * BLOCK + tid;
       uint32_t p = e / K, s = e - p * K;
-      const uint32_t* wo = &sb.wsum[(j * WARPS + warp) * 3];
+      const uint32_t* wo = &sb.wsum[(j * WARPS + warp) * 4];
       uint32_t c = sb.prefix.v[0] + wo[0] + ex[j][0];
       uint32_t start = sb.prefix.v[1] + wo[1] + ex[j][1];
       uint32_t vpos = sb.prefix.v[2] + wo[2] + ex[j][2];
       uint32_t far = v[j].idx;
       if (cval[j][2]) ws.vout[bp.h + vpos] = far;
       if (c >= segcap) continue;  // overflow: reported by the finalising tile
+      // round 1 claims output per tile (padded to 4 records per tile and
+      // child): room for that padding before the second side's children
+      if (bp.root && c > 0) start += ws.slack;
+      if (!bp.root && pad_next) {
+        // DEAD records from the last record of the segment to its span
+        uint32_t* ri = ws.ri[out_b] + (size_t)s * rcap + __ldg(&par_start[p]);
+        for (uint32_t r = v[j].cnt; r < cval[j][1]; r++) ri[r] = DEAD;
+      }
       segstart[c] = start;
       seg_phys[c] = (uint64_t)s * rcap + __ldg(&par_start[p]);  // where K2 wrote child (p, s)
 #pragma unroll
@@ -228,7 +242,8 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
         // point_in_triangle(a, b, far): -eps * edge_length(.,.) per edge;
         // the (a, b) clause always holds for live points (classify2), so
         // only the two edges to the new apex are needed
-        g.nt_ab = 0.0;
+        g.d_af = sub(Ay, F[1]);
+        g.d_fb = sub(F[1], By);
         g.nt_bf = mul(-eps, edge_length(Bx, By, F[0], F[1]));
         g.nt_fa = mul(-eps, edge_length(F[0], F[1], Ax, Ay));
         g.fidx = far;
@@ -266,6 +281,10 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
     if (last_tile && tid == 0) {
       Sum3 T = s3_combine(sb.prefix, sb.agg);
       uint32_t nseg_next = T.v[0], n_next = T.v[1], emitted = T.v[2];
+      // live points of the next round: records minus the DEAD padding the
+      // round kernel claimed (quickhull.py's compact count)
+      const uint32_t n_true_next = T.v[3] - st->dead_round;
+      if (bp.root && nseg_next > 1) n_next += ws.slack;
       uint32_t status = st->status;
       uint32_t round_next = bp.round + 1;  // the round the children belong to
       // every block has read this round's parameters before they change
@@ -286,8 +305,8 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
       }
       if (DIM == 3 && round_next - 1 < MAX_TRACE) st->tr_flat[round_next - 1] = nseg_next - emitted;
       if (!bp.root && bp.round - 1 < MAX_TRACE) {  // loop round bp.round: (live, kept, segments)
-        st->tr_live[bp.round - 1] = bp.n_live;
-        st->tr_kept[bp.round - 1] = n_next;
+        st->tr_live[bp.round - 1] = bp.n_true;
+        st->tr_kept[bp.round - 1] = n_true_next;
         st->tr_nseg[bp.round - 1] = bp.nseg;
       }
       uint32_t h_next = bp.h + emitted;
@@ -304,7 +323,10 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
       rp.cur = out_b;
       rp.h = h_next;
       rp.round = round_next;
+      rp.n_true = n_true_next;
+      rp.aligned = pad_next ? 1u : 0u;
       rp.pad = 0;
+      st->dead_round = 0;
       st->rp = rp;
       st->status = status;
       st->h_final = h_next;

@@ -59,6 +59,14 @@ constexpr uint32_t ST_NONFINITE = 8;
 
 constexpr uint32_t FL_COLLINEAR = 1;
 
+// Original index of a padding record.  The streaming round kernel claims
+// output in multiples of 4 records (16-byte aligned runs, written by bulk
+// copies) and fills the rest of a claim with DEAD records; the bookkeeping
+// kernel pads every segment to a multiple of 4 the same way.  Every round
+// kernel drops DEAD records on read, and the per-round traces count live
+// records only.  (Original indices are < 2^31.)
+constexpr uint32_t DEAD = 0xFFFFFFFFu;
+
 // Farthest-point aggregate of a run of points (one child segment).
 // Larger `hi` (order-preserving bits of the distance) wins, ties go to the
 // lowest original index (quickhull.py:93-100: first max in a segment whose
@@ -97,11 +105,15 @@ SH_HD Sum3 s3_combine(Sum3 a, Sum3 b) {
 }
 
 // 2D segment: directed split edge a->b (points lie left of it), its
-// farthest point f and the three pre-scaled triangle thresholds
-// (-eps)*|edge| of point_in_triangle (geometry.py:150-156).
+// farthest point f, the constant terms of the two cross products a point is
+// classified with (cross2(a, f, q) and cross2(f, b, q), geometry.py:121:
+// ay - fy and fy - by) and the two pre-scaled triangle thresholds
+// (-eps)*|edge| of point_in_triangle (geometry.py:150-156).  Pairs are laid
+// out for 16-byte shared-memory loads.
 struct __align__(16) Seg2 {
-  double ax, ay, bx, by, fx, fy;
-  double nt_ab, nt_bf, nt_fa;
+  double ax, ay, fx, fy, bx, by;
+  double d_af, d_fb;
+  double nt_bf, nt_fa;
   uint32_t fidx, pad;
 };
 
@@ -131,6 +143,8 @@ struct RoundParams {
   uint32_t cur;           // ping-pong index of the buffers the round reads
   uint32_t h;             // vertices emitted before this round's children
   uint32_t round;         // 0: first split, r: loop round r
+  uint32_t n_true;        // live points entering the round (n_live counts DEAD padding too)
+  uint32_t aligned;       // segments start 4-record aligned: k_stream may take the round (k_book)
   uint32_t pad;
 };
 
@@ -149,7 +163,7 @@ struct DevState {
   int64_t* out_idx;       // user output (device), capacity n
   int32_t* out_facets;    // 3D facet triples (device), NULL = not requested
   int64_t facet_cap;      // triples out_facets can hold
-  uint32_t long_min_live; // k_round_long thresholds (sh_round1.cuh; env overrides for tests)
+  uint32_t long_min_live; // k_stream long-round thresholds (long_round(); env overrides for tests)
   uint32_t long_seg_min;
   // ---- first split (K0/K0b) ----
   double eps;
@@ -173,7 +187,7 @@ struct DevState {
   uint32_t ctr_red;       // last-block counter for reductions
   uint32_t book_small;    // K3 runs in one block (few children); set by K2
   uint32_t nonfinite;     // K0 saw a NaN / inf coordinate
-  uint32_t pad1;
+  uint32_t dead_round;    // DEAD padding records written by the current round (k_stream)
   // ---- traces (per round r, index r-1) ----
   uint32_t tr_live[MAX_TRACE];
   uint32_t tr_kept[MAX_TRACE];
@@ -206,13 +220,24 @@ struct Workspace {
   double* red;               // per block partial records
   uint32_t red_blocks;
   uint32_t round_grid;
-  uint32_t round1_grid;
   uint32_t book_grid;
   uint32_t max_tiles;     // round tiles at capacity
   cudaGraphConditionalHandle cond;
   uint32_t use_cond;
-  uint32_t peeled;        // launch outside the WHILE loop (first rounds): k_round_long may take the round
+  uint32_t peeled;        // launch outside the WHILE loop (first rounds): k_stream may take the round
+  uint32_t slack;         // round 1: extra room before side 1's children (their claims are padded per tile)
+  uint32_t stream_grid;   // k_stream launch: CTAs, points per tile
+  uint32_t stream_T;
 };
+
+// Rounds >= 2 whose segments are long run the streaming kernel
+// (k_stream<SRC_REC>, sh_stream.cuh); the others run k_round.  The first
+// LONG_PEEL loop rounds are launched outside the CUDA graph's WHILE node as
+// the pair (k_stream, k_round), exactly one of which works; inside the WHILE
+// node only k_round runs, so the later, short rounds pay no extra launch.
+constexpr uint32_t LONG_SEG_MIN = 4096;
+constexpr uint32_t LONG_MIN_LIVE = 4u << 20;
+constexpr int LONG_PEEL = 3;  // rounds 2..4 are launched outside the WHILE loop
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long pow2_dev(unsigned long long x) {
@@ -389,6 +414,29 @@ __device__ __forceinline__ void atomic_max_key(Key128* p, uint64_t hi, uint32_t 
     if (!(hi > old.hi || (hi == old.hi && (unsigned long long)idx < old.lo))) return;
     cmp = old;
   }
+}
+
+// thresholds come with the call parameters (defaults LONG_MIN_LIVE /
+// LONG_SEG_MIN; SH_LONG_MIN_LIVE / SH_LONG_SEG_MIN override them, which the
+// tests use to drive every peeled round through k_stream)
+__device__ __forceinline__ bool long_round(const RoundParams& rp, const DevState* st) {
+  return rp.round >= 2 && rp.aligned && rp.n_live >= st->long_min_live &&
+         (uint64_t)rp.n_live >= (uint64_t)st->long_seg_min * rp.nseg;
+}
+
+// Decided by the bookkeeping kernel before it lays out the segments of
+// round `round_next` (from bounds it knows up front): whether that round may
+// run k_stream, i.e. its segments are padded to 4-record alignment.  Padding
+// and k_stream's per-tile DEAD claims grow the positions of the rounds
+// after it; they must stay within the record streams (rcap).
+__device__ __forceinline__ bool stream_eligible(const Workspace& ws, const DevState* st, const RoundParams& bp,
+                                                uint32_t round_next, uint32_t K) {
+  if (round_next < 2 || round_next > 1u + (uint32_t)LONG_PEEL) return false;
+  if (bp.n_true < st->long_min_live || (uint64_t)bp.n_true < (uint64_t)st->long_seg_min * K * bp.nseg) return false;
+  const uint64_t nseg_next = (uint64_t)K * bp.nseg;
+  const uint64_t u = (uint64_t)bp.n_true + st->dead_round + 3 * nseg_next;  // positions of round_next
+  const uint64_t tiles = u / ws.stream_T + nseg_next + 2ull * ws.stream_grid;
+  return u + 3ull * (2 * K) * tiles <= ws.rcap;  // + k_stream's DEAD claims
 }
 
 }  // namespace sh

@@ -25,8 +25,8 @@
 #include "sh_filter3.cuh"
 #include "sh_kernels.cuh"
 #include "sh_prims.cuh"
-#include "sh_round1.cuh"
 #include "sh_round.cuh"
+#include "sh_stream.cuh"
 
 using namespace sh;
 
@@ -59,9 +59,8 @@ struct sh_ctx {
   size_t red_bytes = 0;
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[4];
-  int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0, round1_occ2 = 0, round1_occ3 = 0;
-  int lean1_occ2 = 1, lean1_occ3 = 1;  // k_round1 blocks per SM
-  int long_occ2 = 1, long_occ3 = 1;    // k_round_long blocks per SM
+  int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0;
+  int stream_occ2 = 1, stream_occ3 = 1;  // k_stream blocks per SM
   uint32_t last_n = 0;
   bool last_facets = false;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
@@ -153,11 +152,29 @@ static void free_ws(sh_ctx* c) {
   c->segcap = 0;
 }
 
+// Round 1 claims its output per tile, padded to 4 records per tile and
+// child (sh_stream.cuh); the first-split sides' children are interleaved in
+// the input, so side 0's children may outgrow side 0's span by 3 records
+// per tile: side 1's children start this much later (a multiple of 4).
+static uint32_t round1_slack(int dim, uint64_t n) {
+  const uint64_t T = dim == 2 ? StreamCfg<2>::T : StreamCfg<3>::T;
+  return (uint32_t)(((3 * ((n + T - 1) / T) + 4) + 3) & ~3ull);
+}
+
+// Records per stream: n live points, both sides' round-1 padding, and 1/16
+// headroom for the DEAD records of the streamed rounds (k_book only lets
+// k_stream take a round whose padding fits, stream_eligible()), rounded to a
+// multiple of 16 so every stream starts 64-byte aligned.
+static uint64_t record_cap(int dim, uint64_t n) {
+  return (n + n / 16 + 4096 + 2 * (uint64_t)round1_slack(dim, n) + 15) & ~15ull;
+}
+
 static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mcap) {
   free_ws(c);
   Workspace& w = c->ws;
   const int K = dim;
-  uint64_t rcap = n + 16;
+  w.slack = round1_slack(dim, n);
+  uint64_t rcap = record_cap(dim, n);
   w.rcap = rcap;
   uint64_t max_tiles = (n + RTILE - 1) / RTILE + 4;
   uint64_t book_tiles = ((uint64_t)K * segcap + TILE3 - 1) / TILE3 + 4;
@@ -191,7 +208,8 @@ static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mc
   CK(cudaMemset(w.st, 0, sizeof(DevState)));
   w.max_tiles = (uint32_t)max_tiles;
   w.round_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round_occ2 : c->round_occ3));
-  w.round1_grid = (uint32_t)(c->nsm * (dim == 2 ? c->round1_occ2 : c->round1_occ3));
+  w.stream_grid = (uint32_t)(c->nsm * (dim == 2 ? c->stream_occ2 : c->stream_occ3));
+  w.stream_T = dim == 2 ? StreamCfg<2>::T : StreamCfg<3>::T;
   w.book_grid = (uint32_t)(c->nsm * (dim == 2 ? c->book_occ2 : c->book_occ3));
   c->dim = dim;
   c->cap_n = n;
@@ -228,7 +246,8 @@ static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   // exactly one of the two round kernels does the work (long_round())
   prof_begin(c, s);
   if (SH_LEAN_LONG && ws.peeled)
-    k_round_long<DIM><<<c->nsm * (DIM == 2 ? c->long_occ2 : c->long_occ3), R1B, 0, s>>>(ws);
+    k_stream<DIM, SRC_REC><<<ws.stream_grid, StreamCfg<DIM>::NTHREADS,
+                             StreamCfg<DIM>::SMEM, s>>>(ws);
   k_round<DIM, MODE_NORMAL><<<ws.round_grid, RB, dsm, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
@@ -267,14 +286,8 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   // round 1 re-reads the input and applies the first split on the fly, so
   // the split's survivors are never written
   prof_begin(c, s);
-#ifndef SH_LEAN_R1
-#define SH_LEAN_R1 1
-#endif
-  if (SH_LEAN_R1) {
-    k_round1<DIM><<<c->nsm * (DIM == 2 ? c->lean1_occ2 : c->lean1_occ3), R1B, 0, s>>>(ws);
-  } else {
-    k_round<DIM, MODE_ROUND1><<<ws.round1_grid, RB, dsm, s>>>(ws);
-  }
+  k_stream<DIM, SRC_INPUT><<<ws.stream_grid, StreamCfg<DIM>::NTHREADS,
+                             StreamCfg<DIM>::SMEM, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
   prof_begin(c, s);
@@ -529,37 +542,28 @@ int sh_create(int device, sh_ctx** out) {
   sh_ctx* c = new sh_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  cudaFuncSetAttribute(k_round<2, MODE_ROUND1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)RoundSmem<2>::bytes());
   cudaFuncSetAttribute(k_round<2, MODE_NORMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<2>::bytes());
-  cudaFuncSetAttribute(k_round<3, MODE_ROUND1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)RoundSmem<3>::bytes());
   cudaFuncSetAttribute(k_round<3, MODE_NORMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)RoundSmem<3>::bytes());
-  int o2 = 0, o3 = 0, ob = 0;
-  int o2b = 0, o3b = 0;
+  int o2 = 0, o3 = 0, ob = 0, ob2 = 0, of = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_round<2, MODE_NORMAL>, RB, RoundSmem<2>::bytes());
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_round<3, MODE_NORMAL>, RB, RoundSmem<3>::bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2b, k_round<2, MODE_ROUND1>, RB, RoundSmem<2>::bytes());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3b, k_round<3, MODE_ROUND1>, RB, RoundSmem<3>::bytes());
-  c->round1_occ2 = std::max(1, o2b);
-  c->round1_occ3 = std::max(1, o3b);
-  int ob2 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_book<3>, BLOCK, 0);
-  int of = 0, l2 = 0, l3 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l2, k_round1<2>, R1B, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&l3, k_round1<3>, R1B, 0);
-  int g2 = 0, g3 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g2, k_round_long<2>, R1B, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g3, k_round_long<3>, R1B, 0);
-  c->long_occ2 = std::max(1, g2);
-  c->long_occ3 = std::max(1, g3);
-  c->lean1_occ2 = std::max(1, l2);
-  c->lean1_occ3 = std::max(1, l3);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob2, k_book<2>, BLOCK, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_fac_wrap, FAC_BLOCK, 0);
   c->fac_occ = std::max(1, of);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob2, k_book<2>, BLOCK, 0);
+  cudaFuncSetAttribute(k_stream<2, SRC_INPUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StreamCfg<2>::SMEM);
+  cudaFuncSetAttribute(k_stream<2, SRC_REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StreamCfg<2>::SMEM);
+  cudaFuncSetAttribute(k_stream<3, SRC_INPUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StreamCfg<3>::SMEM);
+  cudaFuncSetAttribute(k_stream<3, SRC_REC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StreamCfg<3>::SMEM);
+  {
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_stream<2, SRC_REC>, StreamCfg<2>::NTHREADS, StreamCfg<2>::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_stream<3, SRC_REC>, StreamCfg<3>::NTHREADS, StreamCfg<3>::SMEM);
+    c->stream_occ2 = std::max(1, a);
+    c->stream_occ3 = std::max(1, b);
+  }
   c->round_occ2 = std::max(1, o2);
   c->round_occ3 = std::max(1, o3);
   c->book_occ3 = std::max(1, std::min(ob, 4));
@@ -599,7 +603,7 @@ int64_t sh_workspace_bytes(int dim, int64_t n) {
   // mirrors alloc_ws / filter_alloc with the default capacities (the
   // workspace only grows past them when a hull overflows, see hull_sync)
   if ((dim != 2 && dim != 3) || n <= 0) return -1;
-  const uint64_t K = dim, rcap = (uint64_t)n + 16;
+  const uint64_t K = dim, rcap = record_cap(dim, (uint64_t)n);
   const uint64_t segcap = default_segcap(dim, (uint64_t)n);
   const uint64_t max_tiles = ((uint64_t)n + RTILE - 1) / RTILE + 4;
   (void)max_tiles;

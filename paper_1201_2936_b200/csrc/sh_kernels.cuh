@@ -85,6 +85,8 @@ __device__ __forceinline__ void start_first_split(DevState* st) {
   rp.cur = 0;
   rp.h = st->h_final;
   rp.round = 0;
+  rp.n_true = st->n;
+  rp.aligned = 0;
   rp.pad = 0;
   st->rp = rp;
 }
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
     st->arrive_book = 0;
     st->book_small = 1;
     st->nonfinite = 0;
+    st->dead_round = 0;
     st->ctr_red = 0;
     st->dmax_bits = 0;
     st->rp.active = 0;

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
 #ifndef SH_LEAN_LONG
 #define SH_LEAN_LONG 1
 #endif
-  if (!R1 && SH_LEAN_LONG && ws.peeled && long_round(rp, st)) return;  // k_round_long (sh_round1.cuh) runs it
+  if (!R1 && SH_LEAN_LONG && ws.peeled && long_round(rp, st)) return;  // k_stream (sh_stream.cuh) runs it
   if (blockIdx.x == 0 && tid == 0) {
     st->ctr_book = 0;  // K3's tile counter
     st->arrive_book = 0;
@@ -488,6 +488,10 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
         }
       } else {
         const uint32_t qi = si[i];
+        if (qi == DEAD) {  // padding record (sh_common.cuh)
+          wv[j] = w;
+          return;
+        }
         if constexpr (DIM == 2) s = classify2(seg_of(w), qx, qy, qi, &dn);
         else s = classify3(seg_of(w), qx, qy, qz, qi, &dn);
       }
