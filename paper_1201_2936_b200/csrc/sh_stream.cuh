@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
   __shared__ uint32_t s_coff[S][NK + 1];  // per stage: stage offset of each child's run (multiples of 4), total
   __shared__ long long s_gdst[S][NK];      // per stage: global element of the first record of child k's run
   __shared__ unsigned long long s_bh[NW][NK];
+  __shared__ uint32_t s_thr[NW][8];        // per warp: running farthest key of child k, upper 32 bits (key 7: never)
   __shared__ uint32_t s_bi[NW][NK];
   __shared__ uint32_t s_rlo[NW];           // per warp: segment of part 0 of the running keys
 
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
     (&s_bi[0][0])[e] = 0xFFFFFFFFu;
   }
   if (tid < NW) s_rlo[tid] = NONE;
+  for (int e = tid; e < NW * 8; e += blockDim.x) (&s_thr[0][0])[e] = (e % 8) < NK ? 0u : 0xFFFFFFFFu;
   __syncthreads();
 
   auto stage_ptr = [&](uint32_t s) { return dsm + (size_t)s * C::STAGE; };
@@ -248,6 +250,9 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
       mbar_wait(&s_ready[su], (u / S) & 1u);
       const unsigned char* sp = stage_ptr(su);
       bool any = false;
+#ifdef SH_DIAG_NOFLUSH
+      return;
+#endif
 #pragma unroll 1
       for (int k = 0; k < NK; k++) {
         const uint32_t c0 = s_coff[su][k], n = s_coff[su][k + 1] - c0;
@@ -261,7 +266,9 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
       }
       if (any) {
         bulk_commit();
+#ifndef SH_DIAG_NOWAIT
         bulk_wait_read<0>();
+#endif
       }
     };
     // the CTA's positions [t0*T, t1*T): fixed T-point tiles of the input;
@@ -408,15 +415,6 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
       }
     }
   };
-  // smallest running farthest key (upper 32 bits) over the warp's children:
-  // a point below it can not be any child's farthest point
-  auto min_thr = [&]() {
-    uint32_t m = 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = 0; k < NK; k++) m = min(m, (uint32_t)(s_bh[warp][k] >> 32));
-    return m;
-  };
-  uint32_t minthr = 0;
 
   // classification of point i of a tile (the reference's fp64 order); returns
   // the child key (part * K + state) or 7 (dropped) and the child's distance
@@ -476,8 +474,10 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
             for (int s2 = 0; s2 < K; s2++) {
               s_bh[warp][s2] = s_bh[warp][K + s2];
               s_bi[warp][s2] = s_bi[warp][K + s2];
+              s_thr[warp][s2] = s_thr[warp][K + s2];
               s_bh[warp][K + s2] = 0ull;
               s_bi[warp][K + s2] = 0xFFFFFFFFu;
+              s_thr[warp][K + s2] = 0u;
             }
           } else {
             if (rlo != NONE) merge_running(0, 2);
@@ -485,12 +485,12 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
             for (int k = 0; k < NK; k++) {
               s_bh[warp][k] = 0ull;
               s_bi[warp][k] = 0xFFFFFFFFu;
+              s_thr[warp][k] = 0u;
             }
           }
           s_rlo[warp] = d.lo;
         }
         __syncwarp();
-        minthr = min_thr();
       }
       const uint32_t h0x = d.sh[0][0], h0y = d.sh[0][1], h0z = d.sh[0][2], h0i = d.sh[0][3];
       const uint32_t h1x = d.sh[1][0], h1i = d.sh[1][3];
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
           if (SRC == SRC_REC && I[it] == DEAD) key = 7u;  // padding record
           // dn > 0 for every survivor: the raw bits order like ordered_bits
           const uint32_t hu = (uint32_t)__double2hiint(dn) | 0x80000000u;
-          candmask |= (key < (uint32_t)NK && hu >= minthr) ? (1u << it) : 0u;
+          candmask |= (hu >= s_thr[warp][key]) ? (1u << it) : 0u;  // reaches the child's running maximum
           const uint32_t shf = 4u * key;
           kr[it] = key | (((nib >> shf) & 15u) << 4);
           nib += 1u << shf;
@@ -579,10 +579,10 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
           if (lane == 0 && (h > ch || (h == ch && mi < ci))) {
             s_bh[warp][k] = h;
             s_bi[warp][k] = mi;
+            s_thr[warp][k] = mu;
           }
           __syncwarp();
         }
-        minthr = min_thr();
       }
     }
 
