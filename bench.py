@@ -1,6 +1,7 @@
 """Benchmark of the B200 Quickhull hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+                    [--scaling weak|strong]
 
 A "step" is one whole hull of the configured workload: every Quickhull
 round of it, from the first bbox/extreme pass to the last vertex, as ONE
@@ -10,25 +11,38 @@ Default workload (N=1): BASELINE.json configs[1] = C2, 2D Quickhull of 100M
 points uniform in the unit disk (fp64, reference generator, seed 0).  The
 other configs are parity cases (tests/), selectable here with --config.
 
+N GPUs (--gpus N): one process per GPU over NCCL.  Without a launcher
+(WORLD_SIZE unset) bench.py starts its own N ranks through
+torch.distributed.run.  Every rank hulls a contiguous slice with the whole
+input's statistics exchanged by one NCCL all-gather, then the candidate
+records are all-gathered and rank 0 hulls their union
+(paper_1201_2936_b200/sharded.py).  --scaling weak (default; C5: strong):
+each rank owns the configured n points (N*n in total); strong: the
+configured n points in total, n/N per rank -- BASELINE config C5 is 200M
+points total over 1/2/4/8 GPUs.  value = total points / max-rank time.
+
 value     Mpoints/s = n * K / (device time of K hulls), input resident in HBM
           (1.6 GB, far larger than the 126 MB L2, so no flush is needed).
 e2e       same metric through the public API with HOST (pinned) buffers:
           H2D copy of the points + hull + D2H of the vertex indices per step.
-roofline  the fused round kernel (k_round): algorithmic bytes of each launch
-          over its CUDA-event duration, measured in an event-instrumented pass
+roofline  the round kernels: algorithmic bytes of each launch over its
+          CUDA-event duration, measured in an event-instrumented pass
           (launch mode 2) right after the timed region; peak =
           MEASURED_PEAKS.json hbm_gbs.  Bytes per launch (R_d = 8*dim + 4):
           first split 8*dim*n (read only); round 1 8*dim*n + R_d*n_2 (it
           re-reads the input instead of a materialised split); round r >= 2
           R_d*(n_r + n_{r+1}).  whole_hull_frac uses SURVEY.md §8(d)'s
-          canonical B_alg (materialised split), which this design undercuts.
+          canonical B_alg (materialised first split), which this design undercuts.
+clocks    nvidia-ml samples every 2 ms through the warm-up, the timed region
+          and a clock window of further steps (at least 1 s of load).
 cpu_baseline  the oracle (single-threaded C restatement of the reference
-          drivers) on the same workload, rank 0, N=1 only.
+          drivers; 3D: its loop + Qhull on the candidates standing in for the
+          reference's LP filter) on the same workload, rank 0, N=1 only.
 
 --impl reference: the reference's CPU implementation of the path -- here the
 oracle port, since the reference is pure Python and cannot travel to the GPU
-box -- timed on a bounded sample of the same workload (the first 10M points of
-the same cloud), rank 0 only.
+box -- on the same workload (the whole cloud when one run takes at most a few
+seconds; otherwise a bounded prefix of it, marked same_config false), rank 0.
 """
 
 import argparse
@@ -58,7 +72,9 @@ CONFIGS = {
     "C4b": ("C4: 3D Quickhull, 10M points uniform in unit ball (fp64)", "uniform-ball", 10_000_000),
     "C5": ("C5: 3D Quickhull, 200M points uniform in ball (fp64)", "uniform-ball", 200_000_000),
 }
-REF_SAMPLE = 10_000_000
+# the reference arm hulls the whole cloud when the port needs at most a few
+# seconds for it (C1-C4); C5 (200M 3D points, ~25 s per run) is sampled
+REF_SAMPLE = {"C5": 20_000_000}
 
 KID_ROUND_FIRST, KID_ROUND = 3, 4
 
@@ -71,54 +87,51 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
-
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled every 2 ms from a thread
+    (nvidia-ml; nvidia-smi's 100 ms period is longer than a timed region)
+    between start() and stop() (B200_PROFILING.md's clock record)."""
 
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.run = False
+        self.t = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.t = None
+            return
+        self.run = True
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+        def loop():
+            bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                    "sw_power_cap": 0x4}
+            while self.run:
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
+                    self.rows.append((sm, [k for k, v in bits.items() if r & v], util))
+                except Exception:
+                    pass
+                time.sleep(0.002)
+        self.t = threading.Thread(target=loop, daemon=True)
+        self.t.start()
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.proc.terminate()
-        self.proc.wait()
+        if self.t is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-ml unavailable"], "samples": 0}
+        self.run = False
         self.t.join(timeout=2)
-
-        def num(v):
-            try:
-                return float(v)
-            except ValueError:
-                return None
-        sm = [num(r[0]) for r in self.rows if num(r[0])]
-        mx = [num(r[1]) for r in self.rows if num(r[1])]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[1]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx,
+                "reasons": reasons, "samples": len(self.rows), "period_ms": 2}
 
 
 def measured_peak():
@@ -206,17 +219,33 @@ def measure_roofline(L, ctx, device, launch, n, dim, config, hull_ms):
             "kernel_ms_by_kind": kernel_ms_by_kind}
 
 
+def clock_window(clk, step, seconds=1.0):
+    """Keep the GPU busy with more (untimed) steps so the clock record covers
+    at least ``seconds`` of load."""
+    import torch
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        step()
+        torch.cuda.synchronize()
+    return clk.stop()
+
+
 def run_sharded(args, ws, rank, local):
-    """N GPUs, weak scaling: rank r hulls points [r*n, (r+1)*n) of one N*n
-    cloud of the configured kind; the global hull is assembled by
-    paper_1201_2936_b200.sharded (NCCL all-reduce of the bbox, all-gather of
-    the per-rank hull vertices, rank-0 merge).  value = N*n / max-rank time."""
+    """N GPUs: rank r hulls a contiguous slice of the cloud; the global hull
+    is assembled by paper_1201_2936_b200.sharded (one NCCL all-gather of the
+    slices' statistics -> global eps and first split on the device, the
+    local hulls, an all-gather of the candidate records, the rank-0 merge).
+    weak: n points per rank (N*n total); strong: n points in total.
+    value = total points / max-rank time."""
     import torch
     import torch.distributed as dist
     from paper_1201_2936_b200 import sharded
 
     desc, kind, n = CONFIGS[args.config]
-    cols = gen(kind, n, start=rank * n)
+    scaling = args.scaling or ("strong" if args.config == "C5" else "weak")
+    n_total = n if scaling == "strong" else n * ws
+    b0, b1 = (n_total * rank) // ws, (n_total * (rank + 1)) // ws
+    cols = gen(kind, b1 - b0, start=b0)
     dim = len(cols)
     host = tuple(torch.from_numpy(c).pin_memory() for c in cols)
     d = tuple(h.to("cuda", non_blocking=True) for h in host)
@@ -224,13 +253,12 @@ def run_sharded(args, ws, rank, local):
     stream = torch.cuda.current_stream()
 
     def step(inp):
-        r = sharded.hull_sharded(inp, rank * n, return_info=True)
-        return r
+        return sharded.hull_sharded(inp, b0, return_info=True)
 
-    for _ in range(args.warmup):
-        res, info = step(d)
     clk = Clocks(local)
     clk.start()
+    for _ in range(args.warmup):
+        res, info = step(d)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     dist.barrier()
     torch.cuda.synchronize()
@@ -240,12 +268,12 @@ def run_sharded(args, ws, rank, local):
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     dist.barrier()
-    clocks = clk.stop()
+    clocks = clock_window(clk, lambda: step(d))
     tot = torch.tensor([sum(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))],
                        dtype=torch.float64, device="cuda")
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     tot_ms = float(tot.item())
-    value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
+    value = n_total * args.steps / (tot_ms / 1e3) / 1e6
     # e2e: pinned host slices in, global indices out on rank 0
     e2e_ms = []
     for i in range(min(args.steps, 3) + 1):
@@ -263,7 +291,7 @@ def run_sharded(args, ws, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if i:
             e2e_ms.append(float(t.item()))
-    e2e_val = n * ws / (statistics.mean(e2e_ms) / 1e3) / 1e6
+    e2e_val = n_total / (statistics.mean(e2e_ms) / 1e3) / 1e6
     # round-kernel roofline of this rank's local hull (same kernels as N=1,
     # with the global eps), measured on rank 0
     roofline = None
@@ -273,63 +301,95 @@ def run_sharded(args, ws, rank, local):
         L, ctx = _lib.lib(), _lib.context(local)
         f = P.hull_indices_2d if dim == 2 else P.hull_indices_3d
         tol = P.Tolerance(eps_abs=info["eps"])
-        roofline = measure_roofline(L, ctx, local, lambda: f(d, tol), n, dim, args.config,
+        roofline = measure_roofline(L, ctx, local, lambda: f(d, tol), b1 - b0, dim, args.config,
                                     tot_ms / args.steps)
     launches = None
     if roofline:
-        # per rank and step: bbox (3 kernels) + the local hull (as in main());
-        # rank 0's merge hull of the gathered candidates is not counted
+        # per rank and step: stats + stats reduction, the local hull (as in
+        # main()), rank 0's merge hull of the gathered candidates (not counted)
         r = roofline["launches"] - 1
-        launches = args.steps * (3 + 5 + 2 * r + min(3, max(0, r - 1)) + (12 if dim == 3 else 0))
+        launches = args.steps * (2 + 4 + 2 * r + min(3, max(0, r - 1)) + (12 if dim == 3 else 0))
     if rank == 0:
         h = int(res.numel())
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc + f", x{ws} ranks: {n:,} points per GPU (weak scaling)",
-                           "n_per_gpu": n, "n_total": n * ws, "dim": dim, "hull": h,
+                "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc + (f", {n_total:,} points over {ws} GPU(s) (strong scaling)"
+                                               if scaling == "strong" else
+                                               f", x{ws} ranks: {n:,} points per GPU (weak scaling)"),
+                           "n_total": n_total, "n_per_gpu": b1 - b0, "dim": dim, "hull": h,
                            "union_candidates": info["union"],
                            "l2": "inputs larger than the 126 MB L2; no flush",
-                           "parallelism": f"dp{ws}: contiguous index shards, NCCL all-reduce of the "
-                                          "bbox + all-gather of shard hull vertices, rank-0 merge"},
+                           "parallelism": f"dp{ws}: contiguous index slices; one NCCL all-gather of the "
+                                          "slice statistics (bbox + lexicographic extremes) -> global eps "
+                                          "and first split on the device; all-gather of the candidate "
+                                          "records; rank-0 merge hull"},
                 "e2e": {"value": round(e2e_val, 2), "unit": UNIT,
-                        "h2d_bytes_per_step": 8 * dim * n * ws, "d2h_bytes_per_step": 8 * h,
+                        "h2d_bytes_per_step": 8 * dim * n_total, "d2h_bytes_per_step": 8 * h,
                         "ms_per_step": round(statistics.mean(e2e_ms), 3)},
                 "gpu_launches": launches, "roofline": roofline, "cpu_baseline": None, "clocks": clocks}
         print(json.dumps(line), flush=True)
 
 
+def reference_run(dim, cols):
+    """One run of the CPU reference port on ``cols``: the oracle's 2D driver,
+    or its 3D loop + Qhull on the candidates (the stand-in for the
+    reference's LP filter)."""
+    import oracle
+    if dim == 2:
+        r = oracle.hull2d(*cols)
+    else:
+        r = oracle.full_hull3d(*cols)[0]
+    assert r.status == 0
+    return r
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
-    import oracle
     desc, kind, n = CONFIGS[args.config]
-    m = min(n, REF_SAMPLE)
+    m = min(n, REF_SAMPLE.get(args.config, n))
     cols = gen(kind, m)
-    fn = oracle.hull2d if len(cols) == 2 else oracle.hull3d
+    dim = len(cols)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        r = fn(*cols)
+        reference_run(dim, cols)
         dt = time.perf_counter() - t0
-        assert r.status == 0
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
     value = m * len(times) / tot / 1e6
-    sample = (f"first {m:,} points of the {args.config} cloud (same generator/seed) per step; "
-              f"single-threaded C restatement of the reference drivers (oracle/qh_oracle.c)")
+    what = ("the whole cloud" if m == n else f"the first {m:,} points of the cloud (same generator/seed)")
+    sample = (f"{what} per step; single-threaded C restatement of the reference drivers "
+              f"(oracle/qh_oracle.c)" + ("" if dim == 2 else "; 3D: its loop + Qhull on the candidates "
+                                         "standing in for the reference's LP filter"))
     line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * tot / len(times), 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "n": m, "sample_of": n},
+            "config": {"workload": desc, "n": m, "same_config": m == n, **({} if m == n else {"sample_of": n})},
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n):
+    """bench.py --gpus N without a launcher: run N ranks of this script
+    through torch.distributed.run (one process per GPU) and pass rank 0's
+    line through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ, SH_BENCH_CHILD="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -343,13 +403,17 @@ def main():
     ap.add_argument("--facets", action="store_true",
                     help="3D configs: also build the facet triples inside every step")
     ap.add_argument("--sharded", action="store_true",
-                    help="use the multi-GPU (sharded) pipeline even at N=1")
+                    help="use the multi-GPU (sharded) pipeline even at N=1 (C5 always does)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="multi-GPU work split (default: strong for C5, weak otherwise)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
 
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if args.gpus > 1 and ws == 1 and not os.environ.get("SH_BENCH_CHILD"):
+        sys.exit(spawn_ranks(args.gpus))
 
     import torch
     import torch.distributed as dist
@@ -359,10 +423,11 @@ def main():
     from paper_1201_2936_b200 import _lib
 
     torch.cuda.set_device(local)
-    if ws > 1 or args.sharded:
-        # NCCL's version banner goes to stdout, where rank 0 must print one
-        # JSON line only
-        os.environ.setdefault("NCCL_DEBUG", "WARN")
+    if ws > 1 or args.sharded or args.config == "C5":
+        # NCCL's log (communicator ranks, NVLS/NVLink paths) goes to stderr:
+        # rank 0 prints one JSON line on stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
@@ -412,6 +477,8 @@ def main():
             r = P.hull_indices_3d(pts, facets=want_fac)
             return r[0] if want_fac else r
     f(d)
+    clk = Clocks(local)
+    clk.start()
     for _ in range(args.warmup):
         launch()
     torch.cuda.synchronize()
@@ -419,8 +486,6 @@ def main():
     rounds, h = int(res.iterations), int(res.h)
 
     # ---------------- timed region: K whole hulls, device-timed
-    clk = Clocks(local)
-    clk.start()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     barrier()
     torch.cuda.synchronize()
@@ -430,7 +495,7 @@ def main():
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     barrier()
-    clocks = clk.stop()
+    clocks = clock_window(clk, launch)
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     tot_ms = sum(step_ms)
     if ws > 1:
@@ -468,15 +533,14 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        import oracle
-        fn = oracle.hull2d if dim == 2 else oracle.hull3d
         t0 = time.perf_counter()
-        r = fn(*cols)
+        reference_run(dim, cols)
         dt = time.perf_counter() - t0
-        assert r.status == 0 and len(r.idx) == res.candidates
         cpu = {"value": round(n / dt / 1e6, 3), "unit": UNIT, "cores": 1, "kind": "port",
                "sample": f"the whole {args.config} workload ({n:,} points), one run, "
-                         "single-threaded C restatement of the reference drivers (oracle/)"}
+                         "single-threaded C restatement of the reference drivers (oracle/)" +
+                         ("" if dim == 2 else "; 3D: its loop + Qhull on the candidates standing in "
+                                              "for the reference's LP filter")}
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,

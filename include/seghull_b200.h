@@ -105,6 +105,31 @@ int64_t sh_trace(sh_ctx* ctx, int64_t* live, int64_t* kept, int64_t* nseg, int64
 int sh_bbox(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride, int64_t n,
             int dim, double* out, void* stream);
 
+/* Sharded hulls (paper_1201_2936_b200/sharded.py).
+ *
+ * sh_stats: one pass over a slice -> out (device, SH_STATS = 14 doubles):
+ * -min x, -min y, -min z, max x, max y, max z (a MAX all-reduce merges the
+ * boxes of all slices), then the lexicographic minimum and maximum
+ * (quickhull.py:75-84) as (x, y, z, global index = gidx_offset + local),
+ * z = 0 in 2D.  Stream-ordered, no host synchronisation.
+ * sh_stats_reduce: gathered (device, world x 14, every rank's sh_stats) ->
+ * out (device, 14): the whole input's box and lexicographic extremes.
+ * sh_set_shard: the next hull calls on this context use the whole input's
+ * statistics gstats (device, 14 doubles, read on the device -- the host
+ * never waits for them): flag SH_SHARD_EPS: eps = eps_rel * hypot(spans of
+ * the global box) (Tolerance.effective of the whole input, geometry.py:
+ * 79-83); flag SH_SHARD_SPLIT: the first split uses the global
+ * lexicographic extremes; one that lies in another slice enters this
+ * slice's hull as a virtual point, reported as local index n (min) or n + 1
+ * (max).  gstats = NULL clears the setting. */
+#define SH_STATS 14
+#define SH_SHARD_EPS 1
+#define SH_SHARD_SPLIT 2
+int sh_stats(sh_ctx* ctx, const double* x, const double* y, const double* z, int64_t stride, int64_t n, int dim,
+             int64_t gidx_offset, double* out, void* stream);
+int sh_stats_reduce(sh_ctx* ctx, const double* gathered, int world, int dim, double* out, void* stream);
+int sh_set_shard(sh_ctx* ctx, const double* gstats, int64_t gidx_offset, int flags);
+
 /* Device bytes the context allocates for `dim`-D hulls of n points with the
  * default table capacities: the ping-pong record streams (2 * dim streams of
  * (8*dim + 4)-byte records, capacity n each) plus segment tables sized for

@@ -21,7 +21,9 @@ SH_FLAG_COLLINEAR = 1
 EXPORTED = ("sh_create", "sh_destroy", "sh_hull2d", "sh_hull3d", "sh_hull2d_async",
             "sh_hull3d_async", "sh_fetch", "sh_trace", "sh_reserve", "sh_hypot_host",
             "sh_set_launch_mode", "sh_launch_times", "sh_filter_stats", "sh_bbox", "sh_segmented_scan", "sh_flag_permute",
-            "sh_compact", "sh_scatter", "sh_orient_host", "sh_workspace_bytes", "sh_uniform_points", "sh_facet_stats", "sh_last_error", "sh_version")
+            "sh_compact", "sh_scatter", "sh_orient_host", "sh_workspace_bytes", "sh_uniform_points", "sh_facet_stats",
+            "sh_stats", "sh_stats_reduce", "sh_set_shard", "sh_last_error", "sh_version")
+SH_STATS, SH_SHARD_EPS, SH_SHARD_SPLIT = 14, 1, 2
 
 
 class ShResult(ctypes.Structure):
@@ -32,7 +34,7 @@ class ShResult(ctypes.Structure):
 
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 
 def build(force=False):
@@ -101,6 +103,12 @@ def lib():
             L.sh_facet_stats.restype = ctypes.c_int
             L.sh_filter_stats.argtypes = [P, P, I64]
             L.sh_filter_stats.restype = ctypes.c_int
+            L.sh_stats.argtypes = [P, P, P, P, I64, I64, ctypes.c_int, I64, P, P]
+            L.sh_stats.restype = ctypes.c_int
+            L.sh_stats_reduce.argtypes = [P, P, ctypes.c_int, ctypes.c_int, P, P]
+            L.sh_stats_reduce.restype = ctypes.c_int
+            L.sh_set_shard.argtypes = [P, P, I64, ctypes.c_int]
+            L.sh_set_shard.restype = ctypes.c_int
             L.sh_last_error.argtypes = []
             L.sh_last_error.restype = ctypes.c_char_p
             L.sh_version.argtypes = []
@@ -114,18 +122,29 @@ def last_error():
 
 
 _ctx = {}
+_dev_locks = {}
+
+
+def device_lock(device: int):
+    """The lock serialising use of a device's context: a context (workspace,
+    pinned parameter mirror, captured graphs) is not thread-safe, so every
+    hull call holds it (including the hull + trace pair of quickhull_3d)."""
+    with _lock:
+        lk = _dev_locks.get(device)
+        if lk is None:
+            lk = _dev_locks[device] = threading.RLock()
+        return lk
 
 
 def context(device: int):
-    """One C-ABI context per device (workspace + captured CUDA graphs)."""
+    """One C-ABI context per device (workspace + captured CUDA graphs),
+    created once under the lock."""
     with _lock:
         c = _ctx.get(device)
-    if c is None:
-        h = ctypes.c_void_p()
-        rc = lib().sh_create(device, ctypes.byref(h))
-        if rc != SH_OK:
-            raise RuntimeError(f"sh_create failed ({rc}): {last_error()}")
-        with _lock:
-            _ctx[device] = h
-        c = h
-    return c
+        if c is None:
+            h = ctypes.c_void_p()
+            rc = lib().sh_create(device, ctypes.byref(h))
+            if rc != SH_OK:
+                raise RuntimeError(f"sh_create failed ({rc}): {last_error()}")
+            c = _ctx[device] = h
+        return c

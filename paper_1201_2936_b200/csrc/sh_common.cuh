@@ -59,6 +59,11 @@ constexpr uint32_t ST_NONFINITE = 8;
 
 constexpr uint32_t FL_COLLINEAR = 1;
 
+// sharded hulls: statistics record layout and flags (include/seghull_b200.h)
+constexpr int STATS_N = 14;           // -lo[3], hi[3], lexmin[4], lexmax[4] (SH_STATS)
+constexpr uint32_t SHARD_EPS = 1;     // eps = eps_rel * hypot(spans of the global bbox)
+constexpr uint32_t SHARD_SPLIT = 2;   // first-split line through the global lexicographic extremes
+
 // Original index of a padding record.  The streaming round kernel claims
 // output in multiples of 4 records (16-byte aligned runs, written by bulk
 // copies) and fills the rest of a claim with DEAD records; the bookkeeping
@@ -165,6 +170,13 @@ struct DevState {
   int64_t facet_cap;      // triples out_facets can hold
   uint32_t long_min_live; // k_stream long-round thresholds (long_round(); env overrides for tests)
   uint32_t long_seg_min;
+  // sharded hulls (sh_set_shard): the all-ranks statistics (device, SH_STATS
+  // doubles: -lo[3], hi[3], lex-min and lex-max records (x, y, z, global
+  // index)), this slice's first global index, SHARD_* flags
+  const double* gstats;
+  int64_t gidx_offset;
+  uint32_t shard_flags;
+  uint32_t pad_sh;
   // ---- first split (K0/K0b) ----
   double eps;
   uint32_t imin, imax, ifar;

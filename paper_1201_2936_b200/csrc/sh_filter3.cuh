@@ -220,8 +220,17 @@ __global__ void __launch_bounds__(BLOCK) k_f_gather(Workspace ws, FilterWs f) {
   unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     uint32_t q = ws.vout[i];
-    double c[3] = {ld_coord(st->px, stride, q), ld_coord(st->py, stride, q),
-                   ld_coord(st->pz, stride, q)};
+    double c[3];
+    if (q < st->n) {
+      c[0] = ld_coord(st->px, stride, q);
+      c[1] = ld_coord(st->py, stride, q);
+      c[2] = ld_coord(st->pz, stride, q);
+    } else {  // virtual first-split extreme of a sharded hull (k_first_reduce)
+      const double* v = q == st->n ? st->pa : st->pb;
+      c[0] = v[0];
+      c[1] = v[1];
+      c[2] = v[2];
+    }
     f.cx[i] = c[0];
     f.cy[i] = c[1];
     f.cz[i] = c[2];

@@ -52,6 +52,11 @@ struct sh_ctx {
   uint32_t segcap = 0;   // segments
   uint32_t mcap = 0;     // 3D filter: candidates
   unsigned long long* bbox_bits = nullptr;  // sh_bbox scratch
+  void* stats_parts = nullptr;                // sh_stats scratch: per-block partials + counter
+  // sh_set_shard: applies to every hull call until cleared
+  const double* shard_gstats = nullptr;
+  int64_t shard_offset = 0;
+  uint32_t shard_flags = 0;
   Workspace ws{};
   FilterWs fws{};
   FacetWs facws{};       // 3D facet output (allocated on the first facet request)
@@ -423,6 +428,9 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     h->long_min_live = e1 ? (uint32_t)strtoul(e1, nullptr, 10) : LONG_MIN_LIVE;
     h->long_seg_min = e2 ? (uint32_t)strtoul(e2, nullptr, 10) : LONG_SEG_MIN;
   }
+  h->gstats = c->shard_gstats;
+  h->gidx_offset = c->shard_offset;
+  h->shard_flags = c->shard_gstats ? c->shard_flags : 0u;
   h->out_facets = want_facets ? facets : nullptr;
   h->facet_cap = want_facets ? facet_cap : 0;
   CK(cudaMemcpyAsync(c->ws.st, h, offsetof(DevState, eps), cudaMemcpyHostToDevice, s));
@@ -590,6 +598,7 @@ void sh_destroy(sh_ctx* c) {
   free_ws(c);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->bbox_bits) cudaFree(c->bbox_bits);
+  if (c->stats_parts) cudaFree(c->stats_parts);
   for (auto& e : c->ev0)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->ev1)
@@ -737,6 +746,48 @@ int sh_bbox(sh_ctx* c, const double* x, const double* y, const double* z, int64_
   k_bbox<<<c->nsm * 8, BLOCK, 0, s>>>(x, y, dim == 3 ? z : y, stride, (uint32_t)n, dim, c->bbox_bits);
   k_bbox_final<<<1, 32, 0, s>>>(c->bbox_bits, out, dim);
   CK(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_stats(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride, int64_t n, int dim,
+             int64_t gidx_offset, double* out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if ((dim != 2 && dim != 3) || n <= 0 || !x || !y || (dim == 3 && !z) || !out || stride < 1)
+    return set_err(SH_CONTRACT, "bad stats arguments");
+  if (n >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "n must be < 2^31");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t grid = (uint32_t)c->nsm * 4;
+  if (!c->stats_parts) {
+    CK(cudaMalloc(&c->stats_parts, (size_t)grid * sizeof(FirstRed) + 64));
+    CK(cudaMemset(c->stats_parts, 0, (size_t)grid * sizeof(FirstRed) + 64));
+  }
+  FirstRed* parts = reinterpret_cast<FirstRed*>(c->stats_parts);
+  uint32_t* counter = reinterpret_cast<uint32_t*>(parts + grid);
+  if (dim == 2)
+    k_stats<2><<<grid, BLOCK, 0, s>>>(x, y, y, stride, (uint32_t)n, gidx_offset, parts, counter, out);
+  else
+    k_stats<3><<<grid, BLOCK, 0, s>>>(x, y, z, stride, (uint32_t)n, gidx_offset, parts, counter, out);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_stats_reduce(sh_ctx* c, const double* gathered, int world, int dim, double* out, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if ((dim != 2 && dim != 3) || world < 1 || !gathered || !out) return set_err(SH_CONTRACT, "bad stats arguments");
+  CK(cudaSetDevice(c->device));
+  if (dim == 2) k_stats_reduce<2><<<1, 32, 0, (cudaStream_t)stream>>>(gathered, world, out);
+  else k_stats_reduce<3><<<1, 32, 0, (cudaStream_t)stream>>>(gathered, world, out);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_set_shard(sh_ctx* c, const double* gstats, int64_t gidx_offset, int flags) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (flags & ~3) return set_err(SH_CONTRACT, "unknown shard flags");
+  c->shard_gstats = gstats;
+  c->shard_offset = gidx_offset;
+  c->shard_flags = (uint32_t)flags;
   return SH_OK;
 }
 

@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     if (threadIdx.x != 0) return;
     for (int w = 1; w < WARPS; w++) fr_merge<DIM>(s_w[0], s_w[w]);
   }
-  const FirstRed t = s_w[0];
+  FirstRed t = s_w[0];
   st->ctr_red = 0;
   __threadfence();
   if (*(volatile uint32_t*)&st->nonfinite) {  // ContractViolation, nothing else runs
@@ -267,12 +267,38 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     st->first_active = 0;
     return;
   }
-  // Tolerance.effective: eps_rel * np.hypot.reduce(spans)
-  double acc = sub(t.hi[0], t.lo[0]);
+  // Tolerance.effective: eps_rel * np.hypot.reduce(spans) -- of the whole
+  // input's box when this is one slice of a sharded hull
+  const double* gs = st->gstats;
+  const uint32_t sf = gs ? st->shard_flags : 0u;
+  double lo[3], hi[3];
 #pragma unroll
-  for (int k = 1; k < DIM; k++) acc = glibc_hypot(acc, sub(t.hi[k], t.lo[k]));
+  for (int k = 0; k < 3; k++) {
+    lo[k] = (sf & SHARD_EPS) ? -gs[k] : t.lo[k];
+    hi[k] = (sf & SHARD_EPS) ? gs[3 + k] : t.hi[k];
+  }
+  double acc = sub(hi[0], lo[0]);
+#pragma unroll
+  for (int k = 1; k < DIM; k++) acc = glibc_hypot(acc, sub(hi[k], lo[k]));
   double eps = st->use_eps_abs ? st->eps_abs : mul(st->eps_rel, acc);
   st->eps = eps;
+  if (sf & SHARD_SPLIT) {
+    // the first-split line through the global lexicographic extremes (hull
+    // vertices of the whole input); one from another slice enters this
+    // slice's hull as a virtual point with index n (min) / n + 1 (max)
+    const int64_t off = st->gidx_offset;
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const double* g = gs + 6 + 4 * e;
+      const long long gi = (long long)g[3];
+      LexRec& r = e ? t.mx : t.mn;
+      if (gi != off + (long long)r.idx) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) r.c[k] = g[k];
+        r.idx = n + (uint32_t)e;
+      }
+    }
+  }
   st->imin = t.mn.idx;
   st->imax = t.mx.idx;
   bool same = true;
@@ -479,6 +505,103 @@ __global__ void k_bbox_init(unsigned long long* out, int dim) {
 
 __global__ void k_bbox_final(unsigned long long* out, double* res, int dim) {
   if (threadIdx.x < 2 * dim) res[threadIdx.x] = from_ordered_bits(out[threadIdx.x]);
+}
+
+// ------------------------------------------------------------------ stats
+// One slice of a sharded hull (sh_stats): bbox and lexicographic extremes
+// (quickhull.py:75-84, with global indices) in one pass.  out (SH_STATS
+// doubles): -lo[3], hi[3] (one MAX all-reduce merges boxes), lex-min
+// (x, y, z, global index), lex-max.  Partials per block, last block merges.
+template <int DIM>
+__global__ void __launch_bounds__(BLOCK) k_stats(const double* px, const double* py, const double* pz,
+                                                 int64_t stride, uint32_t n, int64_t offset, FirstRed* parts,
+                                                 uint32_t* counter, double* out) {
+  const double* P[3] = {px, py, pz};
+  FirstRed r;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    r.lo[k] = INFINITY;
+    r.hi[k] = -INFINITY;
+    r.mn.c[k] = INFINITY;
+    r.mx.c[k] = -INFINITY;
+  }
+  r.mn.idx = 0xFFFFFFFFu;
+  r.mx.idx = 0;
+  r.mn.pad = r.mx.pad = 0;
+  for (uint32_t i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
+    LexRec q;
+#pragma unroll
+    for (int k = 0; k < 3; k++) q.c[k] = (k < DIM) ? ld_coord(P[k], stride, i) : 0.0;
+    q.idx = i;
+    q.pad = 0;
+#pragma unroll
+    for (int k = 0; k < DIM; k++) {
+      r.lo[k] = fmin(r.lo[k], q.c[k]);
+      r.hi[k] = fmax(r.hi[k], q.c[k]);
+    }
+    if (lex_less<DIM>(q, r.mn)) r.mn = q;
+    if (lex_less<DIM>(r.mx, q)) r.mx = q;
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    FirstRed o = shfl_xor_t(r, m);
+    fr_merge<DIM>(r, o);
+  }
+  __shared__ FirstRed s_w[WARPS];
+  __shared__ bool s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_w[warp] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < WARPS; w++) fr_merge<DIM>(s_w[0], s_w[w]);
+    parts[blockIdx.x] = s_w[0];
+    __threadfence();
+    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  FirstRed t = ld_cg_fr(parts);
+  for (uint32_t b = 1; b < gridDim.x; b++) {
+    FirstRed o = ld_cg_fr(parts + b);
+    fr_merge<DIM>(t, o);
+  }
+  *counter = 0;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    out[k] = k < DIM ? -t.lo[k] : 0.0;
+    out[3 + k] = k < DIM ? t.hi[k] : 0.0;
+    out[6 + k] = t.mn.c[k];
+    out[10 + k] = t.mx.c[k];
+  }
+  out[9] = (double)(offset + (int64_t)t.mn.idx);
+  out[13] = (double)(offset + (int64_t)t.mx.idx);
+}
+
+// The ranks' statistics (gathered: world x SH_STATS) -> the whole input's:
+// elementwise max of the boxes, lexicographic min / max of the extreme
+// records (coordinates, then global index).
+template <int DIM>
+__global__ void k_stats_reduce(const double* gathered, int world, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double g[STATS_N];
+  for (int k = 0; k < STATS_N; k++) g[k] = gathered[k];
+  auto less = [](const double* a, const double* b) {
+    for (int k = 0; k < DIM; k++) {
+      if (a[k] < b[k]) return true;
+      if (a[k] > b[k]) return false;
+    }
+    return a[3] < b[3];
+  };
+  for (int r = 1; r < world; r++) {
+    const double* o = gathered + (size_t)r * STATS_N;
+    for (int k = 0; k < 6; k++) g[k] = fmax(g[k], o[k]);
+    if (less(o + 6, g + 6))
+      for (int k = 0; k < 4; k++) g[6 + k] = o[6 + k];
+    if (less(g + 10, o + 10))
+      for (int k = 0; k < 4; k++) g[10 + k] = o[10 + k];
+  }
+  for (int k = 0; k < STATS_N; k++) out[k] = g[k];
 }
 
 // ------------------------------------------------------------------ K0b

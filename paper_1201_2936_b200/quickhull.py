@@ -102,11 +102,46 @@ def _as_device_coords(points, dim):
     return [base + 8 * k for k in range(dim)], t.stride(0), n, [t]
 
 
+_out_cache = {}
+
+
+def _out_buffer(device, n):
+    """Per-device scratch for the C ABI's index output (capacity n + 2: two
+    virtual extremes of a sharded hull); callers copy out the h written
+    entries.  Reused across calls (under the device lock) instead of
+    allocating 8 bytes per input point every call."""
+    buf = _out_cache.get(device)
+    if buf is None or buf.numel() < n + 2:
+        buf = _out_cache[device] = torch.empty(max(n + 2, 1024), dtype=torch.int64,
+                                               device=torch.device("cuda", device))
+    return buf
+
+
 def _stream_ptr(device):
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False):
+class _Shard:
+    """sh_set_shard for the duration of one hull call (sharded.py): the whole
+    input's statistics (device tensor, SH_STATS doubles), this slice's first
+    global index, SH_SHARD_* flags."""
+
+    def __init__(self, shard, ctx):
+        self.shard, self.ctx = shard, ctx
+
+    def __enter__(self):
+        if self.shard is not None:
+            gstats, offset, flags = self.shard
+            rc = _lib.lib().sh_set_shard(self.ctx, gstats.data_ptr(), int(offset), int(flags))
+            if rc != _lib.SH_OK:
+                _raise_for(rc)
+
+    def __exit__(self, *exc):
+        if self.shard is not None:
+            _lib.lib().sh_set_shard(self.ctx, None, 0, 0)
+
+
+def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False, shard=None):
     """Original indices (int64 tensor) of the 2D hull vertices.
 
     ``points``: an (n, 2) float64 tensor or a pair of 1-D float64 tensors.
@@ -120,18 +155,20 @@ def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False):
     device = keep[0].device.index
     if n == 0:
         raise EmptyInputError("cannot take the hull of an empty point set")
-    out = torch.empty(n, dtype=torch.int64, device=keep[0].device)
     res = _lib.ShResult()
-    with torch.cuda.device(device):
-        rc = _lib.lib().sh_hull2d(_lib.context(device), ptrs[0], ptrs[1], stride, n, tol.eps_rel,
-                                  tol.eps_abs, out.data_ptr(), ctypes.byref(res), _stream_ptr(device))
+    with torch.cuda.device(device), _lib.device_lock(device):
+        ctx = _lib.context(device)
+        out = _out_buffer(device, n)
+        with _Shard(shard, ctx):
+            rc = _lib.lib().sh_hull2d(ctx, ptrs[0], ptrs[1], stride, n, tol.eps_rel, tol.eps_abs,
+                                      out.data_ptr(), ctypes.byref(res), _stream_ptr(device))
+        idx = out[:res.h].clone() if rc == _lib.SH_OK else None
     if rc != _lib.SH_OK:
         _raise_for(rc)
-    idx = out[:res.h]
     return (idx, res) if return_info else idx
 
 
-def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False):
+def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False, shard=None):
     """Original indices (int64 tensor) of the 3D hull vertices, plus the
     (f, 3) int32 facet triples when ``facets`` is true: original indices,
     counter-clockwise seen from outside, exact (coplanar vertices are
@@ -146,25 +183,27 @@ def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_i
     device = keep[0].device.index
     if n == 0:
         raise EmptyInputError("cannot take the hull of an empty point set")
-    out = torch.empty(n, dtype=torch.int64, device=keep[0].device)
     # facets <= 2 * vertices - 4; start from a size that covers volume-like
     # clouds and retry once with the exact count for surface-like ones
     fcap = min(2 * n + 8, max(4096, 16 * int(n ** 0.5))) if facets else 0
     for _ in range(2):
         fout = torch.empty((max(fcap, 1), 3), dtype=torch.int32, device=keep[0].device)
         res = _lib.ShResult()
-        with torch.cuda.device(device):
-            rc = _lib.lib().sh_hull3d(_lib.context(device), ptrs[0], ptrs[1], ptrs[2], stride, n,
-                                      tol.eps_rel, tol.eps_abs, out.data_ptr(),
-                                      fout.data_ptr() if facets else None, fcap, ctypes.byref(res),
-                                      _stream_ptr(device))
+        with torch.cuda.device(device), _lib.device_lock(device):
+            ctx = _lib.context(device)
+            out = _out_buffer(device, n)
+            with _Shard(shard, ctx):
+                rc = _lib.lib().sh_hull3d(ctx, ptrs[0], ptrs[1], ptrs[2], stride, n, tol.eps_rel,
+                                          tol.eps_abs, out.data_ptr(),
+                                          fout.data_ptr() if facets else None, fcap,
+                                          ctypes.byref(res), _stream_ptr(device))
+            idx = out[:res.h].clone() if rc == _lib.SH_OK else None
         if facets and rc == _lib.SH_CONTRACT and res.facets > fcap:
             fcap = int(res.facets)
             continue
         break
     if rc != _lib.SH_OK:
         _raise_for(rc)
-    idx = out[:res.h]
     fac = fout[:res.facets] if facets else None
     if return_info:
         return idx, fac, res
@@ -177,7 +216,8 @@ def trace(device=None):
     device = torch.cuda.current_device() if device is None else device
     cap = 4096
     arrs = [np.zeros(cap, np.int64) for _ in range(4)]
-    r = _lib.lib().sh_trace(_lib.context(device), *(a.ctypes.data for a in arrs), cap)
+    with _lib.device_lock(device):
+        r = _lib.lib().sh_trace(_lib.context(device), *(a.ctypes.data for a in arrs), cap)
     return np.stack([a[:r] for a in arrs], axis=1)
 
 
@@ -237,13 +277,16 @@ def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance(), facets: bool = 
     ``HullResult.facets`` with the hull's triangles."""
     _validate(points, 3)
     cols = _to_device(points)
-    idx, fac, res = hull_indices_3d(cols, tol, facets=facets, return_info=True)
+    device = cols[0].device.index
+    with _lib.device_lock(device):  # the hull and its trace, as one unit
+        idx, fac, res = hull_indices_3d(cols, tol, facets=facets, return_info=True)
+        tr = trace(device) if res.iterations else None
     idx = idx.cpu().numpy()
     warnings = []
     if res.flags & _lib.SH_FLAG_COLLINEAR:
         warnings.append("collinear input: hull is the two extrema")  # :338
-    if res.iterations:
-        for r, (_, _, _, flat) in enumerate(trace(cols[0].device.index), start=1):
+    if tr is not None:
+        for r, (_, _, _, flat) in enumerate(tr, start=1):
             if flat:
                 warnings.append(f"round {r}: dropped {int(flat)} near-coplanar segment(s)")  # :387-389
     if res.pruned:

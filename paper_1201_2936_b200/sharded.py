@@ -1,42 +1,51 @@
 """Sharded Quickhull across GPUs.
 
 The point cloud is split into contiguous index slices, one per rank (one
-process per GPU).  The ranks exchange only small messages:
+process per GPU).  The ranks exchange only small messages, and the host
+waits for the device only where a size must be known:
 
-  1. every rank computes its slice's bounding box on the device (sh_bbox);
-     an all-reduce (MIN / MAX) gives the whole input's box, and every rank
-     derives the same eps = eps_rel * hypot.reduce(spans), which is exactly
+  1. every rank runs one statistics pass over its slice on the device
+     (sh_stats: bounding box and lexicographic extremes with global indices,
+     quickhull.py:75-84); ONE all-gather (NCCL over NVLink) of these
+     14-double records, reduced on the device (sh_stats_reduce), gives every
+     rank the whole input's box and extreme points;
+  2. every rank hulls its slice with them, read on the device
+     (sh_set_shard): eps = eps_rel * hypot.reduce(global spans) -- exactly
      the reference's Tolerance.effective of the whole input
-     (geometry.py:79-83);
-  2. every rank hulls its slice on its own GPU with that eps (the full
-     single-GPU path, 3D extreme filter included);
-  3. an all-gather of (count) and then of the padded candidate records
-     (coordinates + global index) brings the per-rank hull vertices to
-     every rank;
-  4. rank 0 hulls the union, with the same eps, after sorting it by global
-     index so that the "lowest original index" tie-breaks see the global
-     order.
+     (geometry.py:79-83) -- and the first split along the global extremes
+     (hull vertices of the whole input, entering slices that do not hold them
+     as virtual points), so every rank discards what the whole input's first
+     split discards; the full single-GPU path, 3D extreme filter included;
+  3. one all-gather of (candidate count, status) -- a rank whose slice is
+     degenerate (3D coplanar) contributes all its points, any other failure
+     is raised on every rank instead of leaving the others blocked in a
+     collective -- then an all-gather of the padded candidate records
+     (coordinates + global index);
+  4. rank 0 hulls the union, deduplicated and sorted by global index so that
+     the "lowest original index" tie-breaks see the global order, with the
+     same eps.
 
 hull(all) = hull(union of the shard hulls), so the vertex set equals the
 single-GPU one for inputs in general position (SURVEY.md Appendix A.7 checked
 disk, near-circle, square, ball and cube).  The on-circle config (C3) keeps
 path-dependent eps decisions and must not be sharded.
 
-The exchanged data is tiny (48 B of box, ~10^4-10^5 records of 32 B), so
-the collectives are latency-bound NCCL calls over NVLink; the hull work has
-no collective inside it.  The same code runs over gloo on CPU tensors (tests)
-and in a single-process "loopback" mode that hulls P slices one after the
-other on one GPU (tests, and P-way checking on a 1-GPU box).
+The same code runs over gloo on CPU tensors (tests, with CPU stand-ins for the
+device statistics and hull) and in a single-process "loopback" mode that
+hulls P slices one after the other on one GPU (tests, and P-way checking on a
+1-GPU box).
 """
 
-import ctypes
 import math
 
 import numpy as np
 import torch
 
 from . import _lib
+from .errors import DegenerateInputError
 from .geometry import Tolerance
+
+STATS = _lib.SH_STATS
 
 
 def hypot_reduce(spans):
@@ -58,129 +67,225 @@ def effective_eps(lo, hi, tol: Tolerance):
     return tol.eps_rel * hypot_reduce(spans)
 
 
+def eps_of_stats(gstats, dim, tol: Tolerance):
+    """Tolerance.effective of the whole input from reduced statistics (host)."""
+    g = gstats.cpu().numpy()
+    return effective_eps(-g[:dim], g[3:3 + dim], tol)
+
+
 def _columns(points):
     if isinstance(points, (tuple, list)):
         return tuple(points)
     return tuple(points[:, k] for k in range(points.shape[1]))
 
 
-def device_bbox(cols):
-    """(2*dim,) float64 device tensor: per-axis min then max (own kernel)."""
+def _contiguous(cols):
+    """Unit-stride columns (the C ABI takes one element stride for all of
+    them)."""
+    return tuple(c if c.stride(0) == 1 else c.contiguous() for c in cols)
+
+
+def empty_stats(dim, device):
+    """Statistics of an empty slice: neutral for the reduction."""
+    s = torch.full((STATS,), -math.inf, dtype=torch.float64, device=device)
+    s[6:9] = math.inf   # lex-min record: larger than everything
+    s[9] = math.inf
+    if dim == 2:
+        s[2] = s[5] = 0.0
+    return s
+
+
+def device_stats(cols, offset):
+    """(SH_STATS,) float64 device tensor: sh_stats of this slice (one pass,
+    stream-ordered)."""
+    cols = _contiguous(cols)
     dim = len(cols)
     dev = cols[0].device
-    out = torch.empty(2 * dim, dtype=torch.float64, device=dev)
-    cc = [c.contiguous() if c.stride(0) != cols[0].stride(0) else c for c in cols]
-    stride = cc[0].stride(0)
+    out = torch.empty(STATS, dtype=torch.float64, device=dev)
     with torch.cuda.device(dev):
-        rc = _lib.lib().sh_bbox(_lib.context(dev.index), cc[0].data_ptr(), cc[1].data_ptr(),
-                                cc[2].data_ptr() if dim == 3 else None, stride, cc[0].numel(), dim,
-                                out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+        rc = _lib.lib().sh_stats(_lib.context(dev.index), cols[0].data_ptr(), cols[1].data_ptr(),
+                                 cols[2].data_ptr() if dim == 3 else None, 1, cols[0].numel(), dim,
+                                 int(offset), out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
     if rc != _lib.SH_OK:
-        raise RuntimeError(f"sh_bbox failed ({rc}): {_lib.last_error()}")
+        raise RuntimeError(f"sh_stats failed ({rc}): {_lib.last_error()}")
     return out
 
 
-def device_hull(cols, tol: Tolerance):
-    """Local hull of one slice on its GPU (the product path)."""
+def device_reduce_stats(gathered, dim):
+    """(world, SH_STATS) device tensor -> the whole input's statistics."""
+    gathered = gathered.contiguous()
+    dev = gathered.device
+    out = torch.empty(STATS, dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        rc = _lib.lib().sh_stats_reduce(_lib.context(dev.index), gathered.data_ptr(), gathered.shape[0], dim,
+                                        out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+    if rc != _lib.SH_OK:
+        raise RuntimeError(f"sh_stats_reduce failed ({rc}): {_lib.last_error()}")
+    return out
+
+
+def device_bbox(cols):
+    """(2*dim,) float64 device tensor: per-axis min then max (own kernel)."""
+    dim = len(cols)
+    s = device_stats(cols, 0)
+    return torch.cat([-s[:dim], s[3:3 + dim]])
+
+
+def device_hull(cols, offset, tol: Tolerance, gstats):
+    """Local hull of one slice on its GPU (the product path) with the whole
+    input's statistics: global eps and first-split extremes read on the
+    device.  Returns (global indices, coordinates (k, dim), eps used)."""
     from .quickhull import hull_indices_2d, hull_indices_3d
-    if len(cols) == 2:
-        return hull_indices_2d(tuple(cols), tol)
-    return hull_indices_3d(tuple(cols), tol)
+    cols = _contiguous(cols)
+    dim, n = len(cols), cols[0].numel()
+    flags = _lib.SH_SHARD_SPLIT | (_lib.SH_SHARD_EPS if math.isnan(tol.eps_abs) else 0)
+    shard = (gstats, offset, flags)
+    if dim == 2:
+        idx, res = hull_indices_2d(cols, tol, return_info=True, shard=shard)
+    else:
+        idx, _, res = hull_indices_3d(cols, tol, return_info=True, shard=shard)
+    # virtual points n (global lex-min) and n + 1 (global lex-max): their
+    # records come from the statistics
+    virt = idx >= n
+    coords = torch.stack([c[torch.where(virt, torch.zeros_like(idx), idx)] for c in cols], dim=1)
+    gidx = idx + offset
+    if bool(virt.any()):
+        vrec = gstats[6:].view(2, 4)[(idx - n).clamp(0, 1)]
+        coords = torch.where(virt[:, None], vrec[:, :dim], coords)
+        gidx = torch.where(virt, vrec[:, 3].to(torch.int64), gidx)
+    return gidx, coords, float(res.eps)
 
 
-def _records(cols, idx, offset):
-    """Candidate records: coordinates + global index (exact in fp64 below 2^53)."""
-    parts = [c[idx] for c in cols] + [(idx + offset).to(torch.float64)]
-    return torch.stack(parts, dim=1)
+def device_merge_hull(cols, tol: Tolerance):
+    """The rank-0 hull of the union (plain hull: the union holds the global
+    extremes as real points; tol carries the global eps)."""
+    from .quickhull import hull_indices_2d, hull_indices_3d
+    cols = _contiguous(cols)
+    return hull_indices_2d(cols, tol) if len(cols) == 2 else hull_indices_3d(cols, tol)
 
 
-def _merge(union, dim, eps_rel, eps, local_hull):
-    """Final hull of the gathered records; returns global indices."""
+def _local(cols, offset, tol, gstats, local_hull, device):
+    """(records (k, dim + 1), status, eps, message) of this slice: status 0
+    ok, 1 the slice is degenerate (all its points are sent), 2 failure."""
+    dim, n = len(cols), cols[0].numel()
+    if n == 0:
+        return torch.zeros((0, dim + 1), dtype=torch.float64, device=device), 0, math.nan, ""
+    try:
+        gidx, coords, eps = local_hull(cols, offset, tol, gstats)
+        return torch.cat([coords, gidx.to(torch.float64)[:, None]], dim=1), 0, eps, ""
+    except DegenerateInputError:
+        # a coplanar slice: its points all stay candidates of the merge
+        allp = torch.stack(list(cols) + [torch.arange(offset, offset + n, dtype=torch.float64,
+                                                      device=device)], dim=1)
+        return allp, 1, math.nan, ""
+    except Exception as e:  # reported on every rank, see hull_sharded
+        return torch.zeros((0, dim + 1), dtype=torch.float64, device=device), 2, math.nan, repr(e)
+
+
+def _merge(union, dim, eps, merge_hull):
+    """Final hull of the gathered records (deduplicated, in global index
+    order); returns global indices."""
     if union.shape[0] == 0:
         return torch.empty(0, dtype=torch.int64, device=union.device)
-    union = union[torch.argsort(union[:, dim])]  # global index order
+    union = union[torch.argsort(union[:, dim])]
+    keep = torch.ones(union.shape[0], dtype=torch.bool, device=union.device)
+    keep[1:] = union[1:, dim] != union[:-1, dim]  # a global extreme comes from every slice
+    union = union[keep]
     cols = tuple(union[:, k].contiguous() for k in range(dim))
-    fidx = local_hull(cols, Tolerance(eps_rel, eps_abs=eps))
-    return union[fidx.to(union.device), dim].to(torch.int64)
+    idx = merge_hull(cols, Tolerance(eps_abs=eps))
+    return union[idx.to(union.device), dim].to(torch.int64)
+
+
+def _all_gather(t, group):
+    """(world, *t.shape) tensor of every rank's ``t`` (one collective)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+        return out
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t.contiguous(), group=group)
+    return torch.stack(parts)
 
 
 def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local_hull=None,
-                 local_bbox=None, return_info=False):
+                 local_stats=None, reduce_stats=None, merge_hull=None, return_info=False):
     """Hull of a point cloud sharded over the ranks of ``group``.
 
     points: this rank's slice, an (n_i, dim) float64 tensor or a tuple of dim
-    1-D tensors (CUDA for the product path / NCCL; CPU with gloo when
-    ``local_hull`` and ``local_bbox`` are given).  offset: global index of
-    the slice's first point.  Returns the global vertex indices (int64) on
-    rank 0 and None on the other ranks.
+    1-D tensors (CUDA for the product path / NCCL; CPU with gloo when the
+    stand-ins ``local_hull``, ``local_stats``, ``reduce_stats`` and
+    ``merge_hull`` are given).  offset: global index of the slice's first
+    point.  Returns the global vertex indices (int64) on rank 0 and None on
+    the other ranks; every rank raises if any rank failed.
     """
     import torch.distributed as dist
     cols = _columns(points)
     dim = len(cols)
     local_hull = local_hull or device_hull
-    local_bbox = local_bbox or device_bbox
+    local_stats = local_stats or device_stats
+    reduce_stats = reduce_stats or device_reduce_stats
+    merge_hull = merge_hull or device_merge_hull
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     dev = cols[0].device
-    # 1. global bounding box -> identical eps on every rank
-    if cols[0].numel():
-        bb = local_bbox(cols)
-    else:
-        bb = torch.tensor([math.inf] * dim + [-math.inf] * dim, dtype=torch.float64, device=dev)
-    lo, hi = bb[:dim].clone(), bb[dim:].clone()
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
-    lo_h, hi_h = lo.cpu().tolist(), hi.cpu().tolist()
-    eps = effective_eps(lo_h, hi_h, tol)
-    # 2. local hull with the global eps
-    if cols[0].numel():
-        idx = local_hull(cols, Tolerance(tol.eps_rel, eps_abs=eps)).to(dev)
-    else:
-        idx = torch.empty(0, dtype=torch.int64, device=dev)
-    rec = _records(cols, idx, offset)
-    # 3. all-gather the candidate records (counts first, then padded rows)
-    cnt = torch.tensor([rec.shape[0]], dtype=torch.int64, device=dev)
-    counts = [torch.zeros_like(cnt) for _ in range(world)]
-    dist.all_gather(counts, cnt, group=group)
-    counts = [int(c.item()) for c in counts]
+    # 1. statistics: one pass, one all-gather, reduced on the device
+    st = local_stats(cols, offset) if cols[0].numel() else empty_stats(dim, dev)
+    gstats = reduce_stats(_all_gather(st, group), dim)
+    # 2. local hull with the global eps and first split (device-side)
+    rec, status, eps, msg = _local(cols, offset, tol, gstats, local_hull, dev)
+    # 3. candidate counts and status, then the records
+    cs = torch.tensor([rec.shape[0], status], dtype=torch.int64, device=dev)
+    allcs = _all_gather(cs, group).cpu().tolist()  # the one host read of the exchange
+    if any(s == 2 for _, s in allcs):
+        bad = [r for r, (_, s) in enumerate(allcs) if s == 2]
+        raise RuntimeError(f"sharded hull failed on rank(s) {bad}" + (f": {msg}" if msg else ""))
+    counts = [c for c, _ in allcs]
     cap = max(max(counts), 1)
     pad = torch.zeros((cap, dim + 1), dtype=torch.float64, device=dev)
     pad[:rec.shape[0]] = rec
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)
+    parts = _all_gather(pad, group)
     # 4. rank 0: hull of the union
     result = None
     if rank == 0:
-        union = torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
-        result = _merge(union, dim, tol.eps_rel, eps, local_hull)
+        if math.isnan(eps):
+            eps = eps_of_stats(gstats, dim, tol)
+        union = torch.cat([parts[r, :c] for r, c in enumerate(counts)], dim=0)
+        result = _merge(union, dim, eps, merge_hull)
     if return_info:
         return result, {"eps": eps, "local_candidates": counts, "union": sum(counts)}
     return result
 
 
 def hull_sharded_loopback(points, nshards, tol: Tolerance = Tolerance(), local_hull=None,
-                          local_bbox=None, return_info=False):
+                          local_stats=None, reduce_stats=None, merge_hull=None, return_info=False):
     """The same shard -> merge pipeline for ``nshards`` contiguous slices in
     one process (collectives replaced by their obvious local equivalents)."""
     cols = _columns(points)
     dim = len(cols)
     n = cols[0].numel()
+    dev = cols[0].device
     local_hull = local_hull or device_hull
-    local_bbox = local_bbox or device_bbox
+    local_stats = local_stats or device_stats
+    reduce_stats = reduce_stats or device_reduce_stats
+    merge_hull = merge_hull or device_merge_hull
     bounds = [(n * r) // nshards for r in range(nshards + 1)]
     slices = [tuple(c[bounds[r]:bounds[r + 1]] for c in cols) for r in range(nshards)]
-    boxes = [local_bbox(s) for s in slices if s[0].numel()]
-    lo = torch.stack([b[:dim] for b in boxes]).min(dim=0).values.cpu().tolist()
-    hi = torch.stack([b[dim:] for b in boxes]).max(dim=0).values.cpu().tolist()
-    eps = effective_eps(lo, hi, tol)
-    recs = []
+    stats = [local_stats(s, bounds[r]) if s[0].numel() else empty_stats(dim, dev)
+             for r, s in enumerate(slices)]
+    gstats = reduce_stats(torch.stack(stats), dim)
+    recs, eps = [], math.nan
     for r, s in enumerate(slices):
-        if s[0].numel() == 0:
-            continue
-        idx = local_hull(s, Tolerance(tol.eps_rel, eps_abs=eps)).to(cols[0].device)
-        recs.append(_records(s, idx, bounds[r]))
+        rec, status, e, msg = _local(s, bounds[r], tol, gstats, local_hull, dev)
+        if status == 2:
+            raise RuntimeError(f"sharded hull failed on slice {r}: {msg}")
+        eps = e if math.isnan(eps) else eps
+        recs.append(rec)
+    if math.isnan(eps):
+        eps = eps_of_stats(gstats, dim, tol)
     union = torch.cat(recs, dim=0)
-    result = _merge(union, dim, tol.eps_rel, eps, local_hull)
+    result = _merge(union, dim, eps, merge_hull)
     if return_info:
         return result, {"eps": eps, "local_candidates": [r.shape[0] for r in recs], "union": union.shape[0]}
     return result

@@ -20,22 +20,68 @@ import torch.multiprocessing as mp
 import oracle
 from paper_1201_2936_b200 import sharded
 from paper_1201_2936_b200.datagen import generate
+from paper_1201_2936_b200.errors import DegenerateInputError
 from paper_1201_2936_b200.geometry import Tolerance
 
 
-def cpu_bbox(cols):
-    return torch.tensor([float(c.min()) for c in cols] + [float(c.max()) for c in cols],
-                        dtype=torch.float64)
+def cpu_stats(cols, offset):
+    """Host stand-in for sh_stats: -lo, hi (z = 0 in 2D), lexicographic
+    min / max records (x, y, z, global index), lowest index among ties for
+    the min, highest for the max (quickhull.py:75-84)."""
+    a = [c.numpy() for c in cols]
+    dim = len(a)
+    s = np.zeros(14)
+    for k in range(dim):
+        s[k], s[3 + k] = -a[k].min(), a[k].max()
+    keys = tuple(reversed(a))  # np.lexsort: last key is primary
+    order = np.lexsort(keys)
+    mn = order[0]
+    mx = order[-1]
+    # highest index among full ties for the max
+    ties = np.flatnonzero(np.all([c == c[mx] for c in a], axis=0))
+    mx = ties.max()
+    for k in range(dim):
+        s[6 + k], s[10 + k] = a[k][mn], a[k][mx]
+    s[9], s[13] = offset + mn, offset + mx
+    return torch.from_numpy(s)
 
 
-def cpu_hull(cols, tol):
-    """Oracle stand-in for the device hull (exact reference semantics)."""
+def cpu_reduce_stats(gathered, dim):
+    g = gathered.numpy()
+    out = g[0].copy()
+    out[:6] = g[:, :6].max(axis=0)
+    key = lambda r: tuple(r[:dim]) + (r[3],)
+    out[6:10] = min((r[6:10] for r in g), key=key)
+    out[10:14] = max((r[10:14] for r in g), key=key)
+    return torch.from_numpy(out)
+
+
+def cpu_hull(cols, offset, tol, gstats):
+    """Oracle stand-in for the device hull of a slice (exact reference
+    semantics, with the whole input's eps)."""
+    dim = len(cols)
+    eps = sharded.eps_of_stats(gstats, dim, tol)
+    arrs = [c.numpy() for c in cols]
+    if dim == 2:
+        idx = oracle.hull2d(*arrs, eps_rel=tol.eps_rel, eps_abs=eps).idx
+    else:
+        r, idx, _ = oracle.full_hull3d(*arrs, eps_rel=tol.eps_rel, eps_abs=eps)
+        if r.status == oracle.STATUS_DEGENERATE:
+            raise DegenerateInputError("all points are coplanar")
+    idx = torch.from_numpy(np.asarray(idx, dtype=np.int64).copy())
+    coords = torch.stack([c[idx] for c in cols], dim=1)
+    return idx + offset, coords, eps
+
+
+def cpu_merge(cols, tol):
     arrs = [c.numpy() for c in cols]
     if len(arrs) == 2:
-        r = oracle.hull2d(*arrs, eps_rel=tol.eps_rel, eps_abs=tol.eps_abs)
-        return torch.from_numpy(r.idx.copy())
-    _, idx, _ = oracle.full_hull3d(*arrs, eps_rel=tol.eps_rel, eps_abs=tol.eps_abs)
+        return torch.from_numpy(oracle.hull2d(*arrs, eps_rel=tol.eps_rel, eps_abs=tol.eps_abs).idx.copy())
+    idx = oracle.full_hull3d(*arrs, eps_rel=tol.eps_rel, eps_abs=tol.eps_abs)[1]
     return torch.from_numpy(np.asarray(idx, dtype=np.int64).copy())
+
+
+CPU = dict(local_hull=cpu_hull, local_stats=cpu_stats, reduce_stats=cpu_reduce_stats, merge_hull=cpu_merge)
 
 
 def whole(cols):
@@ -58,8 +104,7 @@ def _worker(rank, world, port, kind, n, q):
     cols = generate(kind, n, 0)
     b = [(n * r) // world for r in range(world + 1)]
     mine = tuple(torch.from_numpy(np.ascontiguousarray(c[b[rank]:b[rank + 1]])) for c in cols)
-    res, info = sharded.hull_sharded(mine, b[rank], Tolerance(), local_hull=cpu_hull,
-                                     local_bbox=cpu_bbox, return_info=True)
+    res, info = sharded.hull_sharded(mine, b[rank], Tolerance(), return_info=True, **CPU)
     if rank == 0:
         q.put((np.sort(res.numpy()), info["eps"]))
     dist.barrier()
@@ -87,12 +132,72 @@ def test_gloo_world2_matches_whole_input(kind, n):
     assert eps == 1e-12 * float(np.hypot.reduce(spans))
 
 
+def _layered_cube(n_side=12):
+    """3D lattice sorted by z: a slice of one z-layer is coplanar."""
+    g = np.arange(n_side, dtype=np.float64)
+    z, y, x = np.meshgrid(g, g, g, indexing="ij")
+    rng = np.random.default_rng(5)
+    jit = lambda a: a + rng.uniform(-1e-3, 1e-3, a.shape) * (a > 0) * (a < n_side - 1)
+    return tuple(np.ascontiguousarray(c.ravel()) for c in (jit(x), jit(y), z))
+
+
+def _worker_cols(rank, world, port, cols, q, fail_rank):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    n = cols[0].size
+    b = [(n * r) // world for r in range(world + 1)]
+    mine = tuple(torch.from_numpy(np.ascontiguousarray(c[b[rank]:b[rank + 1]])) for c in cols)
+    hooks = dict(CPU)
+    if rank == fail_rank:
+        def boom(*a):
+            raise MemoryError("simulated device failure")
+        hooks["local_hull"] = boom
+    try:
+        res = sharded.hull_sharded(mine, b[rank], Tolerance(), **hooks)
+        q.put((rank, "ok", None if res is None else np.sort(res.numpy())))
+    except RuntimeError as e:
+        q.put((rank, "raised", str(e)))
+    dist.destroy_process_group()
+
+
+def _run_world(cols, world, fail_rank=-1):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_cols, args=(r, world, port, cols, q, fail_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (st, v)) for r, st, v in (q.get(timeout=240) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def test_gloo_degenerate_slice_contributes_its_points():
+    # 3 ranks over a 12-layer lattice sorted by z: rank 0's slice is
+    # layers 0-3, a full 3D set; with 12 ranks each slice would be a plane.
+    cols = _layered_cube()
+    n = cols[0].size
+    world = 12  # one coplanar z-layer per rank
+    out = _run_world(cols, world)
+    assert out[0][0] == "ok"
+    assert np.array_equal(out[0][1], whole(cols))
+
+
+def test_gloo_failure_raises_on_every_rank():
+    cols = generate("uniform-ball", 20_000, 2)
+    out = _run_world(cols, 2, fail_rank=1)
+    for r in (0, 1):
+        st, msg = out[r]
+        assert st == "raised" and "rank(s) [1]" in msg
+
+
 @pytest.mark.parametrize("nshards", [1, 3, 8])
 def test_loopback_cpu(nshards):
     for kind, n in (("uniform-disk", 100_000), ("uniform-ball", 30_000)):
         cols = generate(kind, n, 1)
-        got = sharded.hull_sharded_loopback(tuple(torch.from_numpy(c) for c in cols), nshards,
-                                            local_hull=cpu_hull, local_bbox=cpu_bbox)
+        got = sharded.hull_sharded_loopback(tuple(torch.from_numpy(c) for c in cols), nshards, **CPU)
         assert np.array_equal(np.sort(got.numpy()), whole(cols))
 
 
@@ -121,3 +226,50 @@ def test_device_bbox_matches_numpy():
     cols = generate("uniform-ball", 1_000_001, 3)
     bb = sharded.device_bbox(tuple(torch.from_numpy(c).cuda() for c in cols)).cpu().numpy()
     assert np.array_equal(bb, np.array([c.min() for c in cols] + [c.max() for c in cols]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n,offset", [("uniform-disk", 300_001, 0), ("unit-square", 50_000, 7_000_000),
+                                           ("uniform-ball", 200_003, 123), ("unit-cube", 1000, 5)])
+def test_device_stats_match_host(kind, n, offset):
+    cols = generate(kind, n, 4)
+    d = tuple(torch.from_numpy(c).cuda() for c in cols)
+    got = sharded.device_stats(d, offset).cpu().numpy()
+    assert np.array_equal(got, cpu_stats(tuple(torch.from_numpy(c) for c in cols), offset).numpy())
+    # and the reduction over "ranks"
+    parts = [sharded.device_stats(tuple(c[a:b] for c in d), offset + a)
+             for a, b in ((0, n // 3), (n // 3, n - 10), (n - 10, n))]
+    g = sharded.device_reduce_stats(torch.stack(parts), len(cols)).cpu().numpy()
+    assert np.array_equal(g, got)
+
+
+def _nccl_worker(rank, world, port, kind, n, q):
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    cols = generate(kind, n, 0)
+    b = [(n * r) // world for r in range(world + 1)]
+    mine = tuple(torch.from_numpy(np.ascontiguousarray(c[b[rank]:b[rank + 1]])).cuda() for c in cols)
+    res = sharded.hull_sharded(mine, b[rank])
+    if rank == 0:
+        q.put(np.sort(res.cpu().numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+@pytest.mark.parametrize("kind,n", [("uniform-disk", 2_000_000), ("uniform-ball", 1_000_000)])
+def test_nccl_world2_matches_single(kind, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, kind, n, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cols = generate(kind, n, 0)
+    assert np.array_equal(got, whole(cols))
