@@ -130,6 +130,21 @@ int sh_stats(sh_ctx* ctx, const double* x, const double* y, const double* z, int
 int sh_stats_reduce(sh_ctx* ctx, const double* gathered, int world, int dim, double* out, void* stream);
 int sh_set_shard(sh_ctx* ctx, const double* gstats, int64_t gidx_offset, int flags);
 
+/* The same sharded hull in two halves around the exchange, without a
+ * separate statistics pass: sh_hull_shard_begin launches the hull's own
+ * first pass over the slice (bbox + lexicographic extremes), writes the
+ * slice's statistics (as sh_stats) to stats_out and returns without waiting;
+ * the caller all-gathers them (NCCL, same stream) and reduces them
+ * (sh_stats_reduce); sh_hull_shard_end(gstats, flags) runs the rest of the
+ * hull with the whole input's statistics (as sh_set_shard) and returns like
+ * sh_hull2d / sh_hull3d (out_idx capacity n + 2; no facets).  The two calls
+ * belong together: no other hull may run on the context in between. */
+int sh_hull_shard_begin(sh_ctx* ctx, int dim, const double* x, const double* y, const double* z, int64_t stride,
+                        int64_t n, double eps_rel, double eps_abs, int64_t gidx_offset, double* stats_out,
+                        void* stream);
+int sh_hull_shard_end(sh_ctx* ctx, const double* gstats, int flags, int64_t* out_idx, sh_result* res,
+                      void* stream);
+
 /* Device bytes the context allocates for `dim`-D hulls of n points with the
  * default table capacities: the ping-pong record streams (2 * dim streams of
  * (8*dim + 4)-byte records, capacity n each) plus segment tables sized for

@@ -22,7 +22,8 @@ EXPORTED = ("sh_create", "sh_destroy", "sh_hull2d", "sh_hull3d", "sh_hull2d_asyn
             "sh_hull3d_async", "sh_fetch", "sh_trace", "sh_reserve", "sh_hypot_host",
             "sh_set_launch_mode", "sh_launch_times", "sh_filter_stats", "sh_bbox", "sh_segmented_scan", "sh_flag_permute",
             "sh_compact", "sh_scatter", "sh_orient_host", "sh_workspace_bytes", "sh_uniform_points", "sh_facet_stats",
-            "sh_stats", "sh_stats_reduce", "sh_set_shard", "sh_last_error", "sh_version")
+            "sh_stats", "sh_stats_reduce", "sh_set_shard", "sh_hull_shard_begin", "sh_hull_shard_end",
+            "sh_last_error", "sh_version")
 SH_STATS, SH_SHARD_EPS, SH_SHARD_SPLIT = 14, 1, 2
 
 
@@ -109,6 +110,10 @@ def lib():
             L.sh_stats_reduce.restype = ctypes.c_int
             L.sh_set_shard.argtypes = [P, P, I64, ctypes.c_int]
             L.sh_set_shard.restype = ctypes.c_int
+            L.sh_hull_shard_begin.argtypes = [P, ctypes.c_int, P, P, P, I64, I64, D, D, I64, P, P]
+            L.sh_hull_shard_begin.restype = ctypes.c_int
+            L.sh_hull_shard_end.argtypes = [P, P, ctypes.c_int, P, ctypes.POINTER(ShResult), P]
+            L.sh_hull_shard_end.restype = ctypes.c_int
             L.sh_last_error.argtypes = []
             L.sh_last_error.restype = ctypes.c_char_p
             L.sh_version.argtypes = []

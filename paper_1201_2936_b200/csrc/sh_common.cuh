@@ -176,7 +176,8 @@ struct DevState {
   const double* gstats;
   int64_t gidx_offset;
   uint32_t shard_flags;
-  uint32_t pad_sh;
+  uint32_t defer_first;   // two-stage sharded hull: K0 stops after the reduction (k_shard_apply finishes it)
+  double* stats_out;      // two-stage sharded hull: K0 writes this slice's statistics here
   // ---- first split (K0/K0b) ----
   double eps;
   uint32_t imin, imax, ifar;
@@ -200,6 +201,9 @@ struct DevState {
   uint32_t book_small;    // K3 runs in one block (few children); set by K2
   uint32_t nonfinite;     // K0 saw a NaN / inf coordinate
   uint32_t dead_round;    // DEAD padding records written by the current round (k_stream)
+  // K0's reduction of this slice, kept for k_shard_apply (two-stage hull)
+  double keep_lo[3], keep_hi[3], keep_mn[3], keep_mx[3];
+  uint32_t keep_imn, keep_imx;
   // ---- traces (per round r, index r-1) ----
   uint32_t tr_live[MAX_TRACE];
   uint32_t tr_kept[MAX_TRACE];

@@ -63,7 +63,16 @@ struct sh_ctx {
   int fac_occ = 1;
   size_t red_bytes = 0;
   DevState* st_host = nullptr;  // pinned mirror
-  Graph g[4];
+  Graph g[3][4];         // [stage: 0 whole hull, 1 / 2 two-stage sharded hull][2 2D, 3 3D, 1 3D + facets]
+  // sh_hull_shard_begin: the call it started (sh_hull_shard_end finishes it)
+  struct {
+    int dim = 0;
+    const double *x = nullptr, *y = nullptr, *z = nullptr;
+    int64_t stride = 1, n = 0, offset = 0;
+    double eps_rel = 0, eps_abs = 0;
+    bool open = false;
+  } pend;
+  double* stage_stats = nullptr;  // stats_out of the current stage-1 launch
   int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0;
   int stream_occ2 = 1, stream_occ3 = 1;  // k_stream blocks per SM
   uint32_t last_n = 0;
@@ -147,11 +156,12 @@ static void free_ws(sh_ctx* c) {
   facet_free(c->facws);
   w = Workspace{};
   c->fws = FilterWs{};
-  for (auto& g : c->g) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    if (g.graph) cudaGraphDestroy(g.graph);
-    g = Graph{};
-  }
+  for (auto& gs : c->g)
+    for (auto& g : gs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.graph) cudaGraphDestroy(g.graph);
+      g = Graph{};
+    }
   c->dim = 0;
   c->cap_n = 0;
   c->segcap = 0;
@@ -263,9 +273,9 @@ static int launch_body(sh_ctx* c, Workspace ws, cudaStream_t s) {
   return SH_OK;
 }
 
+// stage 1: K0 over the input (a sharded hull stops here for the exchange)
 template <int DIM>
-static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
-  size_t dsm = RoundSmem<DIM>::bytes();
+static int launch_stage1(sh_ctx* c, Workspace ws, cudaStream_t s) {
   prof_begin(c, s);
   k_init<DIM><<<1, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
@@ -274,6 +284,18 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   k_first_reduce<DIM><<<ws.red_blocks, BLOCK, 0, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_FIRST_REDUCE);
+  return SH_OK;
+}
+
+// stage 2: [the whole input's statistics applied,] the first split, round 1
+template <int DIM>
+static int launch_stage2(sh_ctx* c, Workspace ws, cudaStream_t s, bool apply) {
+  if (apply) {
+    prof_begin(c, s);
+    k_shard_apply<DIM><<<1, 32, 0, s>>>(ws);
+    CK(cudaGetLastError());
+    prof_mark(c, s, KID_FIRST_REDUCE);
+  }
   if (DIM == 3) {
     prof_begin(c, s);
     k_line_far<<<ws.red_blocks, BLOCK, 0, s>>>(ws);
@@ -291,8 +313,7 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   // round 1 re-reads the input and applies the first split on the fly, so
   // the split's survivors are never written
   prof_begin(c, s);
-  k_stream<DIM, SRC_INPUT><<<ws.stream_grid, StreamCfg<DIM>::NTHREADS,
-                             StreamCfg<DIM>::SMEM, s>>>(ws);
+  k_stream<DIM, SRC_INPUT><<<ws.stream_grid, StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::SMEM, s>>>(ws);
   CK(cudaGetLastError());
   prof_mark(c, s, KID_ROUND);
   prof_begin(c, s);
@@ -300,6 +321,14 @@ static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s) {
   CK(cudaGetLastError());
   prof_mark(c, s, KID_BOOK);
   return SH_OK;
+}
+
+template <int DIM>
+static int launch_pre(sh_ctx* c, Workspace ws, cudaStream_t s, int stage) {
+  int rc = SH_OK;
+  if (stage != 2) rc = launch_stage1<DIM>(c, ws, s);
+  if (rc || stage == 1) return rc;
+  return launch_stage2<DIM>(c, ws, s, stage == 2);
 }
 
 template <int DIM>
@@ -324,12 +353,24 @@ static int launch_post(sh_ctx* c, Workspace ws, cudaStream_t s, bool facets) {
   return SH_OK;
 }
 
-// graph slots: 2 = 2D, 3 = 3D vertices, 1 = 3D vertices + facets
+// graph slots: [stage][2 = 2D, 3 = 3D vertices, 1 = 3D vertices + facets];
+// stage 0 the whole hull, 1 / 2 the two halves of a sharded hull
 template <int DIM>
-static int build_graph(sh_ctx* c, bool facets = false) {
-  Graph& G = c->g[(DIM == 3 && facets) ? 1 : DIM];
+static int build_graph(sh_ctx* c, bool facets = false, int stage = 0) {
+  Graph& G = c->g[stage][(DIM == 3 && facets) ? 1 : DIM];
   if (G.exec) return SH_OK;
   cudaStream_t s = c->build_stream;
+  if (stage == 1) {  // K0 only: no loop
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = launch_stage1<DIM>(c, c->ws, s);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (rc) return rc;
+    CK(e);
+    CK(cudaGraphInstantiate(&G.exec, graph, 0));
+    G.graph = graph;
+    return SH_OK;
+  }
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   cudaStreamCaptureStatus cs;
   cudaGraph_t cg = nullptr;
@@ -341,7 +382,7 @@ static int build_graph(sh_ctx* c, bool facets = false) {
   Workspace ws = c->ws;
   ws.cond = handle;
   ws.use_cond = 1;
-  int rc = launch_pre<DIM>(c, ws, s);
+  int rc = launch_pre<DIM>(c, ws, s, stage);
   for (int r = 0; rc == SH_OK && SH_LEAN_LONG && r < LONG_PEEL; r++) {
     Workspace wp = ws;
     wp.peeled = 1;
@@ -384,10 +425,10 @@ static int build_graph(sh_ctx* c, bool facets = false) {
 template <int DIM>
 static int hull_async(sh_ctx* c, const double* x, const double* y, const double* z, int64_t stride,
                       int64_t n, double eps_rel, double eps_abs, int64_t* out_idx, int32_t* facets,
-                      int64_t facet_cap, cudaStream_t s, uint32_t segcap_min, uint32_t mcap_min) {
+                      int64_t facet_cap, cudaStream_t s, uint32_t segcap_min, uint32_t mcap_min, int stage = 0) {
   if (n <= 0) return set_err(SH_EMPTY, "cannot take the hull of an empty point set");
   if (n >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "n must be < 2^31");
-  if (!x || !y || (DIM == 3 && !z) || !out_idx) return set_err(SH_CONTRACT, "null pointer");
+  if (!x || !y || (DIM == 3 && !z) || (!out_idx && stage != 1)) return set_err(SH_CONTRACT, "null pointer");
   if (stride < 1) return set_err(SH_CONTRACT, "stride must be >= 1");
   if (!(eps_rel >= 0)) return set_err(SH_CONTRACT, "eps_rel must be nonnegative");
   CK(cudaSetDevice(c->device));
@@ -397,17 +438,19 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
   if (want_facets && facet_cap < 0) return set_err(SH_CONTRACT, "facet_cap must be >= 0");
   if (want_facets && c->facws.mcap < c->mcap) {
     facet_free(c->facws);
-    Graph& g1 = c->g[1];
-    if (g1.exec) cudaGraphExecDestroy(g1.exec);
-    if (g1.graph) cudaGraphDestroy(g1.graph);
-    g1 = Graph{};
+    for (auto& gs : c->g) {
+      Graph& g1 = gs[1];
+      if (g1.exec) cudaGraphExecDestroy(g1.exec);
+      if (g1.graph) cudaGraphDestroy(g1.graph);
+      g1 = Graph{};
+    }
     if (facet_alloc(c->facws, c->mcap)) {
       facet_free(c->facws);
       cudaGetLastError();
       return set_err(SH_NOMEM, "device allocation failed for the facet workspace");
     }
   }
-  rc = build_graph<DIM>(c, want_facets);
+  rc = build_graph<DIM>(c, want_facets, stage);
   if (rc) return rc;
   // call parameters -> device (pinned mirror, one small async copy)
   DevState* h = c->st_host;
@@ -431,12 +474,14 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
   h->gstats = c->shard_gstats;
   h->gidx_offset = c->shard_offset;
   h->shard_flags = c->shard_gstats ? c->shard_flags : 0u;
+  h->defer_first = stage == 1 ? 1u : 0u;
+  h->stats_out = stage == 1 ? c->stage_stats : nullptr;
   h->out_facets = want_facets ? facets : nullptr;
   h->facet_cap = want_facets ? facet_cap : 0;
   CK(cudaMemcpyAsync(c->ws.st, h, offsetof(DevState, eps), cudaMemcpyHostToDevice, s));
   c->last_facets = want_facets;
   if (c->launch_mode == 0) {
-    CK(cudaGraphLaunch(c->g[want_facets ? 1 : DIM].exec, s));
+    CK(cudaGraphLaunch(c->g[stage][want_facets ? 1 : DIM].exec, s));
   } else {
     // host-driven loop: same kernels, one host sync per round (ncu can not
     // attribute kernels inside graphs that contain conditional nodes)
@@ -444,8 +489,11 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     ws.use_cond = 0;
     c->prof_on = (c->launch_mode == 2);
     c->prof_n = 0;
-    rc = launch_pre<DIM>(c, ws, s);
-    if (rc) return rc;
+    rc = launch_pre<DIM>(c, ws, s, stage);
+    if (rc || stage == 1) {
+      c->prof_on = false;
+      return rc;
+    }
     for (int r = 0;; r++) {
       CK(cudaMemcpyAsync(&h->rp, &c->ws.st->rp, sizeof(RoundParams), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -537,6 +585,29 @@ static int ps_launch(PsView v, int op, int exclusive, T* out, cudaStream_t s) {
   cudaFreeAsync(scratch, s);
   if (rc) return set_err(SH_CUDA, std::string("segmented scan launch: ") + cudaGetErrorString(cudaGetLastError()));
   return SH_OK;
+}
+
+template <int DIM>
+static int shard_end(sh_ctx* c, int64_t* out_idx, sh_result* res, cudaStream_t s) {
+  auto& p = c->pend;
+  uint32_t segmin = 0, mmin = 0;
+  for (int attempt = 0; attempt < 8; attempt++) {
+    int rc = SH_OK;
+    if (attempt > 0)  // the workspace grew (and was reset): K0 again
+      rc = hull_async<DIM>(c, p.x, p.y, p.z, p.stride, p.n, p.eps_rel, p.eps_abs, nullptr, nullptr, 0, s,
+                           segmin, mmin, 1);
+    if (!rc)
+      rc = hull_async<DIM>(c, p.x, p.y, p.z, p.stride, p.n, p.eps_rel, p.eps_abs, out_idx, nullptr, 0, s,
+                           segmin, mmin, 2);
+    if (rc) return rc;
+    rc = fetch(c, res, s);
+    const uint32_t stt = c->st_host->status;
+    if (stt != ST_SEG_OVERFLOW && stt != ST_CAND_OVERFLOW) return rc;
+    uint64_t need = (uint64_t)c->st_host->seg_needed * 2 + 1024;
+    if (stt == ST_SEG_OVERFLOW) segmin = (uint32_t)std::min<uint64_t>(need, (uint64_t)p.n + 4);
+    else mmin = (uint32_t)std::min<uint64_t>(need, (uint64_t)p.n + 4);
+  }
+  return set_err(SH_NOMEM, "segment table capacity retries exhausted");
 }
 
 // ---------------------------------------------------------------- C ABI
@@ -789,6 +860,48 @@ int sh_set_shard(sh_ctx* c, const double* gstats, int64_t gidx_offset, int flags
   c->shard_offset = gidx_offset;
   c->shard_flags = (uint32_t)flags;
   return SH_OK;
+}
+
+int sh_hull_shard_begin(sh_ctx* c, int dim, const double* x, const double* y, const double* z, int64_t stride,
+                        int64_t n, double eps_rel, double eps_abs, int64_t gidx_offset, double* stats_out,
+                        void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if ((dim != 2 && dim != 3) || !stats_out) return set_err(SH_CONTRACT, "bad sharded hull arguments");
+  auto& p = c->pend;
+  p.dim = dim;
+  p.x = x;
+  p.y = y;
+  p.z = z;
+  p.stride = stride;
+  p.n = n;
+  p.offset = gidx_offset;
+  p.eps_rel = eps_rel;
+  p.eps_abs = eps_abs;
+  c->shard_gstats = nullptr;
+  c->shard_offset = gidx_offset;
+  c->shard_flags = 0;
+  c->stage_stats = stats_out;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = dim == 2 ? hull_async<2>(c, x, y, nullptr, stride, n, eps_rel, eps_abs, nullptr, nullptr, 0, s, 0, 0, 1)
+                    : hull_async<3>(c, x, y, z, stride, n, eps_rel, eps_abs, nullptr, nullptr, 0, s, 0, 0, 1);
+  c->stage_stats = nullptr;
+  p.open = rc == SH_OK;
+  return rc;
+}
+
+int sh_hull_shard_end(sh_ctx* c, const double* gstats, int flags, int64_t* out_idx, sh_result* res, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (!c->pend.open) return set_err(SH_CONTRACT, "sh_hull_shard_end without sh_hull_shard_begin");
+  if (!gstats || !out_idx || (flags & ~3)) return set_err(SH_CONTRACT, "bad sharded hull arguments");
+  c->pend.open = false;
+  c->shard_gstats = gstats;
+  c->shard_offset = c->pend.offset;
+  c->shard_flags = (uint32_t)flags;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = c->pend.dim == 2 ? shard_end<2>(c, out_idx, res, s) : shard_end<3>(c, out_idx, res, s);
+  c->shard_gstats = nullptr;
+  c->shard_flags = 0;
+  return rc;
 }
 
 int sh_uniform_points(sh_ctx* c, int dim, int64_t n, uint64_t seed, int64_t start, int layout, double* out,

@@ -124,6 +124,78 @@ __global__ void __launch_bounds__(BLOCK) k_init(Workspace ws) {
   }
 }
 
+// K0's conclusion (one thread): eps (Tolerance.effective, geometry.py:
+// 79-83; of the whole input's box for a sharded hull), the lexicographic
+// extremes (quickhull.py:75-84; the global ones for a sharded hull) and the
+// first split's parameters.
+template <int DIM>
+__device__ void finish_first_reduce(Workspace ws, FirstRed t) {
+  DevState* st = ws.st;
+  const uint32_t n = st->n;
+  if (*(volatile uint32_t*)&st->nonfinite) {  // ContractViolation, nothing else runs
+    st->status = ST_NONFINITE;
+    st->h_final = 0;
+    st->first_active = 0;
+    return;
+  }
+  // Tolerance.effective: eps_rel * np.hypot.reduce(spans) -- of the whole
+  // input's box when this is one slice of a sharded hull
+  const double* gs = st->gstats;
+  const uint32_t sf = gs ? st->shard_flags : 0u;
+  double lo[3], hi[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    lo[k] = (sf & SHARD_EPS) ? -gs[k] : t.lo[k];
+    hi[k] = (sf & SHARD_EPS) ? gs[3 + k] : t.hi[k];
+  }
+  double acc = sub(hi[0], lo[0]);
+#pragma unroll
+  for (int k = 1; k < DIM; k++) acc = glibc_hypot(acc, sub(hi[k], lo[k]));
+  double eps = st->use_eps_abs ? st->eps_abs : mul(st->eps_rel, acc);
+  st->eps = eps;
+  if (sf & SHARD_SPLIT) {
+    // the first-split line through the global lexicographic extremes (hull
+    // vertices of the whole input); one from another slice enters this
+    // slice's hull as a virtual point with index n (min) / n + 1 (max)
+    const int64_t off = st->gidx_offset;
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+      const double* g = gs + 6 + 4 * e;
+      const long long gi = (long long)g[3];
+      LexRec& r = e ? t.mx : t.mn;
+      if (gi != off + (long long)r.idx) {
+#pragma unroll
+        for (int k = 0; k < 3; k++) r.c[k] = g[k];
+        r.idx = n + (uint32_t)e;
+      }
+    }
+  }
+  st->imin = t.mn.idx;
+  st->imax = t.mx.idx;
+  bool same = true;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    st->pa[k] = t.mn.c[k];
+    st->pb[k] = t.mx.c[k];
+    if (k < DIM) same = same && (t.mn.c[k] == t.mx.c[k]);
+  }
+  ws.vout[0] = t.mn.idx;
+  if (same) {  // quickhull.py:195-197 / :320-322 -- every point coincides
+    st->h_final = 1;
+    return;
+  }
+  ws.vout[1] = t.mx.idx;
+  st->h_final = 2;
+  if (DIM == 2) {
+    // off_line threshold eps * edge_length(pmin, pmax), quickhull.py:203
+    st->thr_line = mul(eps, edge_length(t.mn.c[0], t.mn.c[1], t.mx.c[0], t.mx.c[1]));
+    st->first_active = 1;
+    start_first_split(st);
+  } else {
+    st->first_active = (n > 2) ? 2u : 0u;  // 2: K0b runs next
+  }
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   DevState* st = ws.st;
@@ -261,68 +333,52 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   FirstRed t = s_w[0];
   st->ctr_red = 0;
   __threadfence();
-  if (*(volatile uint32_t*)&st->nonfinite) {  // ContractViolation, nothing else runs
-    st->status = ST_NONFINITE;
-    st->h_final = 0;
-    st->first_active = 0;
-    return;
-  }
-  // Tolerance.effective: eps_rel * np.hypot.reduce(spans) -- of the whole
-  // input's box when this is one slice of a sharded hull
-  const double* gs = st->gstats;
-  const uint32_t sf = gs ? st->shard_flags : 0u;
-  double lo[3], hi[3];
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    lo[k] = (sf & SHARD_EPS) ? -gs[k] : t.lo[k];
-    hi[k] = (sf & SHARD_EPS) ? gs[3 + k] : t.hi[k];
-  }
-  double acc = sub(hi[0], lo[0]);
-#pragma unroll
-  for (int k = 1; k < DIM; k++) acc = glibc_hypot(acc, sub(hi[k], lo[k]));
-  double eps = st->use_eps_abs ? st->eps_abs : mul(st->eps_rel, acc);
-  st->eps = eps;
-  if (sf & SHARD_SPLIT) {
-    // the first-split line through the global lexicographic extremes (hull
-    // vertices of the whole input); one from another slice enters this
-    // slice's hull as a virtual point with index n (min) / n + 1 (max)
+  if (st->stats_out) {  // this slice's statistics (sh_hull_shard_begin)
+    double* o = st->stats_out;
     const int64_t off = st->gidx_offset;
 #pragma unroll
-    for (int e = 0; e < 2; e++) {
-      const double* g = gs + 6 + 4 * e;
-      const long long gi = (long long)g[3];
-      LexRec& r = e ? t.mx : t.mn;
-      if (gi != off + (long long)r.idx) {
-#pragma unroll
-        for (int k = 0; k < 3; k++) r.c[k] = g[k];
-        r.idx = n + (uint32_t)e;
-      }
+    for (int k = 0; k < 3; k++) {
+      o[k] = k < DIM ? -t.lo[k] : 0.0;
+      o[3 + k] = k < DIM ? t.hi[k] : 0.0;
+      o[6 + k] = t.mn.c[k];
+      o[10 + k] = t.mx.c[k];
     }
+    o[9] = (double)(off + (int64_t)t.mn.idx);
+    o[13] = (double)(off + (int64_t)t.mx.idx);
   }
-  st->imin = t.mn.idx;
-  st->imax = t.mx.idx;
-  bool same = true;
+  if (st->defer_first) {  // k_shard_apply finishes with the whole input's statistics
 #pragma unroll
-  for (int k = 0; k < 3; k++) {
-    st->pa[k] = t.mn.c[k];
-    st->pb[k] = t.mx.c[k];
-    if (k < DIM) same = same && (t.mn.c[k] == t.mx.c[k]);
-  }
-  ws.vout[0] = t.mn.idx;
-  if (same) {  // quickhull.py:195-197 / :320-322 -- every point coincides
-    st->h_final = 1;
+    for (int k = 0; k < 3; k++) {
+      st->keep_lo[k] = t.lo[k];
+      st->keep_hi[k] = t.hi[k];
+      st->keep_mn[k] = t.mn.c[k];
+      st->keep_mx[k] = t.mx.c[k];
+    }
+    st->keep_imn = t.mn.idx;
+    st->keep_imx = t.mx.idx;
     return;
   }
-  ws.vout[1] = t.mx.idx;
-  st->h_final = 2;
-  if (DIM == 2) {
-    // off_line threshold eps * edge_length(pmin, pmax), quickhull.py:203
-    st->thr_line = mul(eps, edge_length(t.mn.c[0], t.mn.c[1], t.mx.c[0], t.mx.c[1]));
-    st->first_active = 1;
-    start_first_split(st);
-  } else {
-    st->first_active = (n > 2) ? 2u : 0u;  // 2: K0b runs next
+  finish_first_reduce<DIM>(ws, t);
+}
+
+// Stage 2 of a two-stage sharded hull: K0's kept reduction + the whole
+// input's statistics (st->gstats) -> eps and the first split.
+template <int DIM>
+__global__ void k_shard_apply(Workspace ws) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DevState* st = ws.st;
+  FirstRed t;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    t.lo[k] = st->keep_lo[k];
+    t.hi[k] = st->keep_hi[k];
+    t.mn.c[k] = st->keep_mn[k];
+    t.mx.c[k] = st->keep_mx[k];
   }
+  t.mn.idx = st->keep_imn;
+  t.mx.idx = st->keep_imx;
+  t.mn.pad = t.mx.pad = 0;
+  finish_first_reduce<DIM>(ws, t);
 }
 
 // ------------------------------------------------------------------ K1

@@ -36,6 +36,7 @@ hulls P slices one after the other on one GPU (tests, and P-way checking on a
 1-GPU box).
 """
 
+import ctypes
 import math
 
 import numpy as np
@@ -146,6 +147,70 @@ def device_hull(cols, offset, tol: Tolerance, gstats):
         idx, _, res = hull_indices_3d(cols, tol, return_info=True, shard=shard)
     # virtual points n (global lex-min) and n + 1 (global lex-max): their
     # records come from the statistics
+    return _globalize(cols, offset, idx, gstats) + (float(res.eps),)
+
+
+class StagedDeviceHull:
+    """The product path of one rank: the local hull in two halves around the
+    statistics exchange (sh_hull_shard_begin / _end), so the statistics come
+    from the hull's own first pass instead of an extra pass over the slice.
+    The device's context is held from begin() to end()."""
+
+    def __init__(self):
+        self.lock = None
+
+    def begin(self, cols, offset, tol: Tolerance):
+        cols = _contiguous(cols)
+        self.cols, self.offset, self.tol = cols, offset, tol
+        dev = cols[0].device
+        self.device = dev.index
+        out = torch.empty(STATS, dtype=torch.float64, device=dev)
+        self.lock = _lib.device_lock(self.device)
+        self.lock.acquire()
+        try:
+            with torch.cuda.device(dev):
+                dim = len(cols)
+                rc = _lib.lib().sh_hull_shard_begin(
+                    _lib.context(self.device), dim, cols[0].data_ptr(), cols[1].data_ptr(),
+                    cols[2].data_ptr() if dim == 3 else None, 1, cols[0].numel(), tol.eps_rel, tol.eps_abs,
+                    int(offset), out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
+            if rc != _lib.SH_OK:
+                from .quickhull import _raise_for
+                _raise_for(rc)
+        except BaseException:
+            self.release()
+            raise
+        return out
+
+    def end(self, cols, offset, tol, gstats):
+        from .quickhull import _out_buffer, _raise_for
+        try:
+            dim, n = len(self.cols), self.cols[0].numel()
+            flags = _lib.SH_SHARD_SPLIT | (_lib.SH_SHARD_EPS if math.isnan(tol.eps_abs) else 0)
+            res = _lib.ShResult()
+            dev = self.cols[0].device
+            with torch.cuda.device(dev):
+                out = _out_buffer(self.device, n)
+                rc = _lib.lib().sh_hull_shard_end(_lib.context(self.device), gstats.data_ptr(), flags,
+                                                  out.data_ptr(), ctypes.byref(res),
+                                                  torch.cuda.current_stream(dev).cuda_stream)
+                if rc != _lib.SH_OK:
+                    _raise_for(rc)
+                idx = out[:res.h].clone()
+        finally:
+            self.release()
+        return _globalize(self.cols, self.offset, idx, gstats) + (float(res.eps),)
+
+    def release(self):
+        if self.lock is not None:
+            self.lock.release()
+            self.lock = None
+
+
+def _globalize(cols, offset, idx, gstats):
+    """Local hull indices (n, n + 1: the virtual global extremes) -> global
+    indices and coordinates (k, dim)."""
+    dim, n = len(cols), cols[0].numel()
     virt = idx >= n
     coords = torch.stack([c[torch.where(virt, torch.zeros_like(idx), idx)] for c in cols], dim=1)
     gidx = idx + offset
@@ -153,7 +218,7 @@ def device_hull(cols, offset, tol: Tolerance, gstats):
         vrec = gstats[6:].view(2, 4)[(idx - n).clamp(0, 1)]
         coords = torch.where(virt[:, None], vrec[:, :dim], coords)
         gidx = torch.where(virt, vrec[:, 3].to(torch.int64), gidx)
-    return gidx, coords, float(res.eps)
+    return gidx, coords
 
 
 def device_merge_hull(cols, tol: Tolerance):
@@ -223,6 +288,12 @@ def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local
     import torch.distributed as dist
     cols = _columns(points)
     dim = len(cols)
+    staged = None
+    if local_hull is None and local_stats is None:
+        # the product path: the statistics come from the hull's own first pass
+        staged = StagedDeviceHull()
+        local_stats = lambda c, o: staged.begin(c, o, tol)
+        local_hull = staged.end
     local_hull = local_hull or device_hull
     local_stats = local_stats or device_stats
     reduce_stats = reduce_stats or device_reduce_stats
@@ -230,11 +301,34 @@ def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     dev = cols[0].device
-    # 1. statistics: one pass, one all-gather, reduced on the device
-    st = local_stats(cols, offset) if cols[0].numel() else empty_stats(dim, dev)
-    gstats = reduce_stats(_all_gather(st, group), dim)
+    # 1. statistics of every slice, one all-gather, reduced on the device
+    begun = True
+    try:
+        st = local_stats(cols, offset) if cols[0].numel() else empty_stats(dim, dev)
+    except Exception as e:  # still take part in the exchange; reported below
+        st, begun, msg0 = empty_stats(dim, dev), False, repr(e)
+    try:
+        gstats = reduce_stats(_all_gather(st, group), dim)
+    except BaseException:
+        if staged:
+            staged.release()
+        raise
     # 2. local hull with the global eps and first split (device-side)
-    rec, status, eps, msg = _local(cols, offset, tol, gstats, local_hull, dev)
+    if begun:
+        rec, status, eps, msg = _local(cols, offset, tol, gstats, local_hull, dev)
+    else:
+        rec, status, eps, msg = torch.zeros((0, dim + 1), dtype=torch.float64, device=dev), 2, math.nan, msg0
+    if staged:
+        staged.release()
+    if world == 1:  # the slice is the whole input: its hull is the answer
+        if status == 2:
+            raise RuntimeError(f"sharded hull failed on rank(s) [0]: {msg}")
+        if status == 1:  # degenerate: the single hull raises the same error
+            merge_hull(cols, tol)
+        result = rec[:, dim].to(torch.int64)
+        if return_info:
+            return result, {"eps": eps, "local_candidates": [rec.shape[0]], "union": rec.shape[0]}
+        return result
     # 3. candidate counts and status, then the records
     cs = torch.tensor([rec.shape[0], status], dtype=torch.int64, device=dev)
     allcs = _all_gather(cs, group).cpu().tolist()  # the one host read of the exchange

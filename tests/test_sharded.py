@@ -273,3 +273,24 @@ def test_nccl_world2_matches_single(kind, n):
         assert p.exitcode == 0
     cols = generate(kind, n, 0)
     assert np.array_equal(got, whole(cols))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n", [("uniform-disk", 3_000_000), ("uniform-ball", 1_000_000),
+                                    ("unit-cube", 200_000), ("near-circle", 500_000)])
+def test_nccl_world1_staged_matches_single(kind, n):
+    """The product path (hull in two stages around the NCCL exchange) on a
+    one-rank communicator: equal to the single hull."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    p = ctx.Process(target=_nccl_worker, args=(0, 1, port, kind, n, q))
+    p.start()
+    got = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    cols = generate(kind, n, 0)
+    d = tuple(torch.from_numpy(c).cuda() for c in cols)
+    import paper_1201_2936_b200 as P
+    single = P.hull_indices_2d(d) if len(cols) == 2 else P.hull_indices_3d(d)
+    assert np.array_equal(got, np.sort(single.cpu().numpy()))
