@@ -15,14 +15,14 @@ from .errors import ContractViolation, DegenerateInputError, EmptyInputError
 from .geometry import PointSet, Tolerance
 from .primitives import (PermutationMap, ScanSpec, compact, flag_permute, head_index_broadcast,
                          reduce_broadcast, scatter, segment_ids, segmented_scan)
-from .quickhull import (HullResult, hull_indices_2d, hull_indices_3d, order_hull_2d, quickhull_2d,
-                        quickhull_3d, trace)
+from .quickhull import (HullResult, filter_stats, hull_indices_2d, hull_indices_3d, order_hull_2d,
+                        quickhull_2d, quickhull_3d, trace)
 from .pointio import PointFileError, generate_device, read_points_device, write_points_binary
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ContractViolation", "DegenerateInputError", "EmptyInputError", "HullResult", "PermutationMap",
+    "ContractViolation", "DegenerateInputError", "EmptyInputError", "HullResult", "PermutationMap", "filter_stats",
     "PointSet", "ScanSpec", "Tolerance", "compact", "flag_permute", "head_index_broadcast",
     "hull_indices_2d", "hull_indices_3d", "order_hull_2d", "quickhull_2d", "quickhull_3d", "reduce_broadcast",
     "scatter", "segment_ids", "segmented_scan", "trace", "PointFileError", "generate_device",

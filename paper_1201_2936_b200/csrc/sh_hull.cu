@@ -62,6 +62,17 @@ struct sh_ctx {
   FacetWs facws{};       // 3D facet output (allocated on the first facet request)
   int fac_occ = 1;
   size_t red_bytes = 0;
+  // the workspace of the other dimension, parked while this one is active
+  // (alternating 2D and 3D hulls neither free nor re-capture anything)
+  struct Parked {
+    int dim = 0;
+    uint64_t cap_n = 0;
+    uint32_t segcap = 0, mcap = 0;
+    Workspace ws{};
+    FilterWs fws{};
+    FacetWs facws{};
+    Graph g[3][4];
+  } parked;
   DevState* st_host = nullptr;  // pinned mirror
   Graph g[3][4];         // [stage: 0 whole hull, 1 / 2 two-stage sharded hull][2 2D, 3 3D, 1 3D + facets]
   // sh_hull_shard_begin: the call it started (sh_hull_shard_end finishes it)
@@ -156,6 +167,7 @@ static void free_ws(sh_ctx* c) {
   facet_free(c->facws);
   w = Workspace{};
   c->fws = FilterWs{};
+  c->facws = FacetWs{};
   for (auto& gs : c->g)
     for (auto& g : gs) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -165,6 +177,7 @@ static void free_ws(sh_ctx* c) {
   c->dim = 0;
   c->cap_n = 0;
   c->segcap = 0;
+  c->mcap = 0;
 }
 
 // Round 1 claims its output per tile, padded to 4 records per tile and
@@ -182,6 +195,20 @@ static uint32_t round1_slack(int dim, uint64_t n) {
 // multiple of 16 so every stream starts 64-byte aligned.
 static uint64_t record_cap(int dim, uint64_t n) {
   return (n + n / 16 + 4096 + 2 * (uint64_t)round1_slack(dim, n) + 15) & ~15ull;
+}
+
+// active workspace <-> parked one
+static void swap_parked(sh_ctx* c) {
+  auto& p = c->parked;
+  std::swap(p.dim, c->dim);
+  std::swap(p.cap_n, c->cap_n);
+  std::swap(p.segcap, c->segcap);
+  std::swap(p.mcap, c->mcap);
+  std::swap(p.ws, c->ws);
+  std::swap(p.fws, c->fws);
+  std::swap(p.facws, c->facws);
+  for (int a = 0; a < 3; a++)
+    for (int b = 0; b < 4; b++) std::swap(p.g[a][b], c->g[a][b]);
 }
 
 static int alloc_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap, uint32_t mcap) {
@@ -247,6 +274,16 @@ static uint32_t default_mcap(uint64_t n) {
 static int ensure_ws(sh_ctx* c, int dim, uint64_t n, uint32_t segcap_min, uint32_t mcap_min) {
   uint32_t want = std::max(default_segcap(dim, n), segcap_min);
   uint32_t mwant = (dim == 3) ? std::max(default_mcap(n), mcap_min) : 0u;
+  if (c->dim != 0 && c->dim != dim) {
+    // park the other dimension's workspace (freeing an older parked one of
+    // this dimension's kind only if it is the one we are about to replace)
+    if (c->parked.dim != dim && c->parked.dim != 0) {
+      swap_parked(c);
+      free_ws(c);
+      swap_parked(c);
+    }
+    swap_parked(c);  // the parked workspace (this dim, or none) becomes active
+  }
   if (c->dim == dim && c->cap_n >= n && c->segcap >= want && c->mcap >= mwant) return SH_OK;
   bool same = c->dim == dim;
   uint64_t cap = std::max<uint64_t>(n, same ? c->cap_n : 0);
@@ -666,6 +703,8 @@ int sh_create(int device, sh_ctx** out) {
 void sh_destroy(sh_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  free_ws(c);
+  swap_parked(c);
   free_ws(c);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->bbox_bits) cudaFree(c->bbox_bits);

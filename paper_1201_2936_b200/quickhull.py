@@ -221,6 +221,42 @@ def trace(device=None):
     return np.stack([a[:r] for a in arrs], axis=1)
 
 
+def hull_warnings(dim, res, trace_rows=None):
+    """The reference's warning strings for a hull result (quickhull.py:208,
+    :308-310, :338, :387-389); ``trace_rows``: trace() of the same hull (3D
+    per-round near-coplanar drops)."""
+    warnings = []
+    if res.flags & _lib.SH_FLAG_COLLINEAR:
+        warnings.append("collinear input: hull is the two x-extrema" if dim == 2
+                        else "collinear input: hull is the two extrema")  # :208 / :338
+    if dim == 3:
+        if trace_rows is not None and res.iterations:
+            for r, (_, _, _, flat) in enumerate(trace_rows, start=1):
+                if flat:
+                    warnings.append(f"round {r}: dropped {int(flat)} near-coplanar segment(s)")  # :387-389
+        if res.pruned:
+            warnings.append(f"pruned {int(res.pruned)} non-extreme candidate vertex(es) emitted by "
+                            "incomplete per-face outside sets")  # :308-310
+    return warnings
+
+
+FILTER_STATS = ("candidates", "grid", "ambiguous", "gjk_capped", "certified", "queries", "scanned",
+                "gjk_iters", "local_pruned", "local_extreme", "global_gjk", "cyc_cert", "cyc_local",
+                "cyc_query", "cyc_global")
+
+
+def filter_stats(device=None):
+    """Diagnostics of the last 3D extreme filter on ``device`` (sh_filter_stats):
+    ``ambiguous`` counts candidates kept because they lie within eps of the
+    other candidates' hull boundary, ``gjk_capped`` those whose GJK hit its
+    iteration cap (both 0 on inputs in general position)."""
+    device = torch.cuda.current_device() if device is None else device
+    out = np.zeros(len(FILTER_STATS), np.int64)
+    with _lib.device_lock(device):
+        k = _lib.lib().sh_filter_stats(_lib.context(device), out.ctypes.data, len(out))
+    return dict(zip(FILTER_STATS[:k], out[:k].tolist()))
+
+
 def _validate(points: PointSet, dim: int):
     # quickhull.py:103-107
     if points.dim != dim:
@@ -241,10 +277,7 @@ def quickhull_2d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
     idx, res = hull_indices_2d(cols, tol, return_info=True)
     idx = idx.cpu().numpy()
     verts = PointSet(tuple(c[idx] for c in points.coords))
-    warnings = []
-    if res.flags & _lib.SH_FLAG_COLLINEAR:
-        warnings.append("collinear input: hull is the two x-extrema")  # :208
-    return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx)
+    return HullResult(verts, int(res.iterations), points.n - verts.n, hull_warnings(2, res), idx)
 
 
 def order_hull_2d(vertices: PointSet) -> PointSet:
@@ -282,16 +315,7 @@ def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance(), facets: bool = 
         idx, fac, res = hull_indices_3d(cols, tol, facets=facets, return_info=True)
         tr = trace(device) if res.iterations else None
     idx = idx.cpu().numpy()
-    warnings = []
-    if res.flags & _lib.SH_FLAG_COLLINEAR:
-        warnings.append("collinear input: hull is the two extrema")  # :338
-    if tr is not None:
-        for r, (_, _, _, flat) in enumerate(tr, start=1):
-            if flat:
-                warnings.append(f"round {r}: dropped {int(flat)} near-coplanar segment(s)")  # :387-389
-    if res.pruned:
-        warnings.append(f"pruned {int(res.pruned)} non-extreme candidate vertex(es) emitted by "
-                        "incomplete per-face outside sets")  # :308-310
+    warnings = hull_warnings(3, res, tr)
     verts = PointSet(tuple(c[idx] for c in points.coords)) if idx.size else PointSet.empty(3)
     return HullResult(verts, int(res.iterations), points.n - verts.n, warnings, idx,
                       fac.cpu().numpy() if fac is not None else None)

@@ -94,6 +94,45 @@ def cases():
                 pts = uniform_box(n, 3, seed) if kind == "unit-cube" else \
                     generate(Distribution(kind, n, seed))
                 out.append((f"{kind}-{n}-s{seed}", pts))
+    out.extend(degenerate_3d())
+    return out
+
+
+def degenerate_3d():
+    """Coplanar / cospherical 3D candidates, where the filter's eps rules
+    decide (quickhull.py:136-164): lattices, points on the faces of a cube,
+    Fibonacci spheres (every point on the sphere), two parallel rings."""
+    out = []
+    for k in (3, 4, 5, 7):
+        g = np.arange(k, dtype=np.float64)
+        z, y, x = np.meshgrid(g, g, g, indexing="ij")
+        out.append((f"lattice-cube-{k}", PointSet((x.ravel().copy(), y.ravel().copy(), z.ravel().copy()))))
+    rng = np.random.default_rng(11)
+    for n in (300, 1500):
+        u = rng.random((n, 2))
+        face = rng.integers(0, 6, n)
+        pts = np.empty((n, 3))
+        for f in range(6):
+            m = face == f
+            ax, sgn = f // 2, float(f % 2)
+            others = [a for a in range(3) if a != ax]
+            pts[m, ax] = sgn
+            pts[m, others[0]] = u[m, 0]
+            pts[m, others[1]] = u[m, 1]
+        out.append((f"cube-faces-{n}", PointSet(tuple(pts[:, j].copy() for j in range(3)))))
+    for n in (200, 1000):
+        i = np.arange(n, dtype=np.float64) + 0.5
+        phi = np.arccos(1.0 - 2.0 * i / n)
+        th = np.pi * (1.0 + 5.0 ** 0.5) * i
+        out.append((f"fibonacci-sphere-{n}", PointSet((np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi),
+                                                       np.cos(phi)))))
+    t = np.linspace(0.0, 2.0 * np.pi, 60, endpoint=False)
+    ring = np.concatenate([t, t])
+    zz = np.concatenate([np.zeros(60), np.ones(60)])
+    inner = rng.random((80, 3)) * 0.5 + 0.25
+    out.append(("rings-120", PointSet((np.concatenate([np.cos(ring), inner[:, 0]]),
+                                        np.concatenate([np.sin(ring), inner[:, 1]]),
+                                        np.concatenate([zz, inner[:, 2]])))))
     return out
 
 

@@ -24,6 +24,10 @@ def test_usage_errors(tmp_path):
     out = str(tmp_path / "x.pts")
     assert cli.main(["gen", "--dist", "uniform-disk", "--n", "10", "--seed", "0", "--dim", "3", "-o", out]) == 2
     assert cli.main(["gen", "--dist", "nope", "--n", "10", "--seed", "0", "--dim", "2", "-o", out]) == 2
+    # Distribution's band check (reference datagen.py:45-46 -> exit code 2)
+    assert cli.main(["gen", "--dist", "near-circle", "--n", "10", "--seed", "0", "--dim", "2", "--band", "1.5",
+                     "-o", out]) == 2
+    assert not os.path.exists(out)
     assert cli.main(["bench", "--dists", "", "--sizes", "10", "--dim", "2", "-o", out]) == 2
     assert cli.main(["bench", "--dists", "uniform-ball", "--sizes", "10", "--dim", "2", "-o", out]) == 2
     assert cli.main(["bench", "--dists", "uniform-disk", "--sizes", "0", "--dim", "2", "-o", out]) == 2

@@ -75,6 +75,11 @@ def _check3(cols, eps_rel=1e-12):
     assert np.array_equal(tr[:, 3], o.flat_counts[:len(tr)])
     assert res.candidates == len(o.idx)
     assert np.array_equal(idx.cpu().numpy(), idx_ref)  # reference discovery order
+    if res.candidates > 4:
+        # general position: no candidate kept for being within eps of the
+        # boundary, and no GJK gave up at its iteration cap
+        fs = P.filter_stats()
+        assert fs["ambiguous"] == 0 and fs["gjk_capped"] == 0, fs
     return res
 
 
@@ -130,6 +135,27 @@ def test_repeat_calls_and_workspace_regrowth():
     assert np.array_equal(a, b)
     _check3(generate("uniform-ball", 50_000, 0))
     _check2(small)
+
+
+def test_alternating_dims_keep_both_workspaces():
+    """2D and 3D hulls alternating on one context park the other
+    dimension's workspace (and its captured graphs) instead of freeing it."""
+    d2 = generate("uniform-disk", 500_000, 3)
+    d3 = generate("uniform-ball", 200_000, 3)
+    r2 = [_check2(d2)[0] for _ in range(2)]
+    r3 = [np.sort(P.hull_indices_3d(dev(d3)).cpu().numpy()) for _ in range(2)]
+    for _ in range(3):
+        assert np.array_equal(_check2(d2)[0], r2[0])
+        assert np.array_equal(np.sort(P.hull_indices_3d(dev(d3)).cpu().numpy()), r3[0])
+    # after warm-up, a switch costs no allocation: time a few alternations
+    import time
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        P.hull_indices_2d(dev(d2))
+        P.hull_indices_3d(dev(d3))
+    torch.cuda.synchronize()
+    assert (time.perf_counter() - t0) / 10 < 0.05
 
 
 def test_many_segments_regrowth():
