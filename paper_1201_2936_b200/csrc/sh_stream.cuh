@@ -687,13 +687,12 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
     for (int it = 0; it < IT; it++) {
       const uint32_t k = kr[it] & 7u;
       const uint32_t w = K == 2 ? ((k & 2u) ? pb[1] : pb[0]) : (k < 2u ? pb[0] : (k < 4u ? pb[1] : pb[K - 1]));
-      const uint32_t pos = ((w >> (16 * (k & 1u))) & 0xFFFFu) + (kr[it] >> 4);
-      if (k < (uint32_t)NK) {
-        sxa[pos] = X[it];
-        sya[pos] = Y[it];
-        if (DIM == 3) sza[pos] = Z[it];
-        sia[pos] = I[it];
-      }
+      // dropped points go to a scratch slot past every staged run (no branch)
+      const uint32_t pos = k < (uint32_t)NK ? ((w >> (16 * (k & 1u))) & 0xFFFFu) + (kr[it] >> 4) : C::CAPD - 1;
+      sxa[pos] = X[it];
+      sya[pos] = Y[it];
+      if (DIM == 3) sza[pos] = Z[it];
+      sia[pos] = I[it];
     }
     // ---- the staged tile is complete once the claims return (next tile)
     fence_proxy_async_smem();
