@@ -1,21 +1,19 @@
-// Kernels of the B200 Quickhull path (2D and 3D), see DESIGN.md.
+// Kernels of the B200 Quickhull path (2D and 3D) around the round kernels,
+// see DESIGN.md.
 //
 //   K0  k_first_reduce  bbox (-> eps, Tolerance.effective geometry.py:79-83)
-//                       + lexicographic extremes (_lex_extreme quickhull.py:75-84)
+//                       + lexicographic extremes (_lex_extreme quickhull.py:75-84);
+//                       for a sharded hull also the slice's statistics, and
+//                       k_shard_apply finishes it with the whole input's
 //   K0b k_line_far      3D third corner: farthest from the extrema line
 //                       (quickhull.py:329-344)
-//   K1  k_round<FIRST>  first split (quickhull.py:200-222 / :346-364)
-//   K2  k_round         one Quickhull round (quickhull.py:224-266 / :366-437):
-//                       simplex discard + child classification + stable
-//                       regroup into K streams + next round's segmented
-//                       farthest point, in ONE read and ONE write of the
-//                       live records, with a decoupled look-back scan that
-//                       carries both the stream offsets and the
-//                       reduce-by-key state of the farthest-point search.
-//   K3  k_book          per-segment bookkeeping (quickhull.py:236-240,
-//                       :268-277 / :380-391, :412-444): dense renumbering
-//                       of occupied children, child edge / face tables,
-//                       vertex emission, device-side termination flag.
+//   K1  k_first_count   first split (quickhull.py:200-222 / :346-364) as a
+//                       counting pass: per side, survivors and farthest point
+//   k_stats / k_stats_reduce / k_bbox: per-slice statistics of sharded hulls
+//
+// The round kernels are k_stream (sh_stream.cuh: round 1 fused with the
+// first split, and every long round) and k_round (sh_round.cuh: the short
+// rounds); the bookkeeping between rounds is k_book (sh_book.cuh).
 #pragma once
 
 #include "sh_common.cuh"

@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     if (uniform && !slow && !R1) {
       const SegT g0 = *reinterpret_cast<const SegT*>(S.seg0[b]);  // staged with the window
 #pragma unroll
-      for (int j = 0; j < RITEMS; j++) classify_item(j, true, [&](uint32_t) -> const SegT& { return g0; });
+      for (int j = 0; j < RITEMS; j++) classify_item(j, true, [&](uint32_t) -> SegT { return g0; });
     } else if (R1) {
 #pragma unroll
       for (int j = 0; j < RITEMS; j++)

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
   using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
   constexpr int K = DIM, NK = 2 * K, NW = C::NW, NT = C::NT, IT = C::IT, T = C::T, S = C::S;
   constexpr uint32_t NONE = 0xFFFFFFFFu;
-  extern __shared__ __align__(128) unsigned char dsm[];
+  extern __shared__ __align__(16) unsigned char dsm[];  // the stages (16-byte aligned bulk copies)
   __shared__ __align__(8) uint64_t s_full[S];
   __shared__ __align__(8) uint64_t s_ready[S];  // staged tile + its claims are in place (NW + 1 arrivals)
   __shared__ StageDesc s_desc[S];
@@ -385,10 +385,6 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
   // ------------------------------------------------------------ consumers
   Key128* slot_key = ws.slot_key;
   uint32_t* cursor = ws.cursor[cur];
-  double* outx = ws.rx[cur ^ 1u];
-  double* outy = ws.ry[cur ^ 1u];
-  double* outz = ws.rz[cur ^ 1u];
-  uint32_t* outi = ws.ri[cur ^ 1u];
   // first-split constants (round 1)
   double f_pa[3], f_pb[3], f_nrm[3];
 #pragma unroll
