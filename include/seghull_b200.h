@@ -145,6 +145,24 @@ int sh_hull_shard_begin(sh_ctx* ctx, int dim, const double* x, const double* y, 
 int sh_hull_shard_end(sh_ctx* ctx, const double* gstats, int flags, int64_t* out_idx, sh_result* res,
                       void* stream);
 
+/* order_hull_2d (reference quickhull.py:449-461) on the device: out_perm
+ * (device, h int64) = the CCW boundary order of the h vertices (x, y device
+ * arrays), starting at the lexicographically smallest, by angle around the
+ * centroid (stable sort).  h < 3: the identity. */
+int sh_order_hull_2d(sh_ctx* ctx, const double* x, const double* y, int64_t h, int64_t* out_perm, void* stream);
+
+/* The CLI's `verify` check (reference oracle.py:20-52, hull2_giftwrap): gift
+ * wrapping from the lexicographic minimum, next vertex = the candidate all
+ * other points lie left of, among candidates collinear within
+ * eps * |cand - cur| the farthest.  Per vertex: a tree reduction of that
+ * rule, a proof that its winner dominates every other point, and an exact
+ * replay of the reference's sequential scan when it does not (ties within
+ * eps), so the walk visits the reference's coordinates.  out_idx (device,
+ * capacity cap) receives the vertex indices in CCW order, *out_h their
+ * count; SH_CONTRACT when cap is too small. */
+int sh_giftwrap_2d(sh_ctx* ctx, const double* x, const double* y, int64_t n, double eps, int64_t* out_idx,
+                   int64_t cap, int64_t* out_h, void* stream);
+
 /* Device bytes the context allocates for `dim`-D hulls of n points with the
  * default table capacities: the ping-pong record streams (2 * dim streams of
  * (8*dim + 4)-byte records, capacity n each) plus segment tables sized for

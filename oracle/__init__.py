@@ -53,8 +53,23 @@ def lib():
         L.oq_hull3d.restype = ctypes.c_int
         L.oq_hull3d.argtypes = [_p, _p, _p, _i64, ctypes.c_double, ctypes.c_double, _p, _p, _p, _p,
                                 _p, _p, _i64, _p, _i64, _p]
+        L.oq_giftwrap2d.restype = _i64
+        L.oq_giftwrap2d.argtypes = [_p, _p, _i64, ctypes.c_double, _p, _i64]
         _lib = L
     return _lib
+
+
+def giftwrap2d(x, y, eps):
+    """hull2_giftwrap (reference seghull/oracle module lines 20-52) in C:
+    indices (first occurrence per coordinate pair), CCW from the
+    lexicographic minimum.  Pinned to the reference by tests/test_checks.py."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.empty(x.size + 1, dtype=np.int64)
+    h = lib().oq_giftwrap2d(_ptr(x), _ptr(y), x.size, float(eps), _ptr(out), out.size)
+    if h < 0:
+        raise ValueError("giftwrap2d: bad arguments")
+    return out[:h]
 
 
 def _ptr(a):

@@ -490,3 +490,47 @@ done3:
   free(segstart); free(segstart2); free(tab); free(tab2); free(far); free(flat);
   return status;
 }
+
+/* hull2_giftwrap (reference seghull/oracle module lines 20-52): sequential
+ * scan in index order, coordinates compared as tuples.  Writes the index of
+ * the first occurrence of each hull vertex, CCW from the lexicographic
+ * minimum; returns the vertex count (or -1 when cap is too small). */
+int64_t oq_giftwrap2d(const double* x, const double* y, int64_t n, double eps, int64_t* out, int64_t cap) {
+  if (n <= 0 || cap < 1) return -1;
+  int64_t s = 0;
+  for (int64_t i = 1; i < n; i++)
+    if (x[i] < x[s] || (x[i] == x[s] && y[i] < y[s])) s = i;
+  int64_t h = 0;
+  out[h++] = s;
+  int64_t cur = s;
+  for (int64_t step = 0; step <= n; step++) {
+    const double cx = x[cur], cy = y[cur];
+    int64_t cand = -1;
+    for (int64_t q = 0; q < n; q++) {
+      if (x[q] == cx && y[q] == cy) continue;
+      if (cand < 0) {
+        cand = q;
+        continue;
+      }
+      const double ax = x[cand] - cx, ay = y[cand] - cy, qx = x[q] - cx, qy = y[q] - cy;
+      const double cr = ax * qy - ay * qx;
+      const double limit = eps * hypot(ax, ay);
+      if (cr < -limit)
+        cand = q;
+      else if (cr <= limit && qx * qx + qy * qy > ax * ax + ay * ay)
+        cand = q;
+    }
+    if (cand < 0 || (x[cand] == x[s] && y[cand] == y[s])) break;
+    if (h >= cap) return -1;
+    /* first occurrence of the coordinates (the reference keeps tuples) */
+    int64_t f = cand;
+    for (int64_t q = 0; q < cand; q++)
+      if (x[q] == x[cand] && y[q] == y[cand]) {
+        f = q;
+        break;
+      }
+    out[h++] = f;
+    cur = cand;
+  }
+  return h;
+}

@@ -27,6 +27,9 @@
 #include "sh_prims.cuh"
 #include "sh_round.cuh"
 #include "sh_stream.cuh"
+#include "sh_order.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 
 using namespace sh;
 
@@ -941,6 +944,96 @@ int sh_hull_shard_end(sh_ctx* c, const double* gstats, int flags, int64_t* out_i
   c->shard_gstats = nullptr;
   c->shard_flags = 0;
   return rc;
+}
+
+int sh_order_hull_2d(sh_ctx* c, const double* x, const double* y, int64_t h, int64_t* out_perm, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (h < 0 || (h > 0 && (!x || !y || !out_perm))) return set_err(SH_CONTRACT, "bad order_hull_2d arguments");
+  if (h >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "h must be < 2^31");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t n = (uint32_t)h;
+  if (n < 3) {  // quickhull.py:455-456: returned as given
+    for (uint32_t i = 0; i < n; i++) {
+      const int64_t v = i;
+      CK(cudaMemcpyAsync(out_perm + i, &v, 8, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return SH_OK;
+  }
+  const uint32_t grid = std::min<uint32_t>((n + BLOCK - 1) / BLOCK, (uint32_t)c->nsm * 4);
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n, 0, 64, s);
+  const size_t bytes = (size_t)n * 24 + (size_t)grid * 16 + 64 + temp + 256;
+  unsigned char* buf = nullptr;
+  CK(cudaMallocAsync((void**)&buf, bytes, s));
+  unsigned long long* k0 = (unsigned long long*)buf;
+  unsigned long long* k1 = k0 + n;
+  uint32_t* v0 = (uint32_t*)(k1 + n);
+  uint32_t* v1 = v0 + n;
+  double* acc = (double*)(((uintptr_t)(v1 + n) + 15) & ~(uintptr_t)15);
+  double* mean = acc + 2 * grid;
+  uint32_t* counter = (uint32_t*)(mean + 2);
+  void* tmp = (void*)(((uintptr_t)(counter + 4) + 255) & ~(uintptr_t)255);
+  CK(cudaMemsetAsync(counter, 0, 4, s));
+  k_ord_sum<<<grid, BLOCK, 0, s>>>(x, y, n, acc, counter, mean);
+  k_ord_keys<<<grid, BLOCK, 0, s>>>(x, y, n, mean, k0, v0);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, v0, v1, (int)n, 0, 64, s);  // stable
+  if (e == cudaSuccess) k_ord_roll<<<1, 1024, 0, s>>>(x, y, n, v1, out_perm);
+  cudaFreeAsync(buf, s);
+  CK(e);
+  CK(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_giftwrap_2d(sh_ctx* c, const double* x, const double* y, int64_t n, double eps, int64_t* out_idx,
+                   int64_t cap, int64_t* out_h, void* stream) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (n <= 0 || !x || !y || !out_idx || !out_h || cap < 1) return set_err(SH_CONTRACT, "bad giftwrap arguments");
+  if (n >= (int64_t)0x7FFFFFF0) return set_err(SH_CONTRACT, "n must be < 2^31");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  // start: the lexicographic minimum (min(pts) in hull2_giftwrap)
+  const uint32_t grid = (uint32_t)std::min<int64_t>((int64_t)c->nsm * 4, (n + BLOCK - 1) / BLOCK);
+  unsigned char* buf = nullptr;
+  CK(cudaMallocAsync((void**)&buf, (size_t)grid * sizeof(GwBest) + 256 + STATS_N * 8, s));
+  GwBest* parts = (GwBest*)buf;
+  GwState* st = (GwState*)(((uintptr_t)(parts + grid) + 15) & ~(uintptr_t)15);
+  double* dstats = (double*)(((uintptr_t)(st + 1) + 15) & ~(uintptr_t)15);
+  int rc = sh_stats(c, x, y, nullptr, 1, n, 2, 0, dstats, stream);
+  if (rc) {
+    cudaFreeAsync(buf, s);
+    return rc;
+  }
+  double stats[STATS_N];
+  CK(cudaMemcpyAsync(stats, dstats, sizeof(stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  GwState h0{};
+  h0.cur = h0.start = (uint32_t)stats[9];
+  h0.h = 1;
+  const int64_t first = h0.start;
+  CK(cudaMemcpyAsync(out_idx, &first, 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(st, &h0, sizeof(h0), cudaMemcpyHostToDevice, s));
+  // at most n + 1 steps (the reference's loop bound); poll between batches
+  GwState hs{};
+  for (int64_t step = 0; step <= n;) {
+    const int64_t batch = std::min<int64_t>(step == 0 ? 8 : 256, n + 1 - step);
+    for (int64_t k = 0; k < batch; k++) {
+      k_gw_step<<<grid, BLOCK, 0, s>>>(x, y, (uint32_t)n, eps, st, parts);
+      k_gw_check<<<grid, BLOCK, 0, s>>>(x, y, (uint32_t)n, eps, st);
+      k_gw_commit<<<1, 1024, 0, s>>>(x, y, (uint32_t)n, eps, st, out_idx, cap);
+    }
+    CK(cudaGetLastError());
+    step += batch;
+    CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hs.done) break;
+  }
+  cudaFreeAsync(buf, s);
+  if (hs.done == 2) return set_err(SH_CONTRACT, "giftwrap output capacity exceeded");
+  *out_h = hs.h;
+  return SH_OK;
 }
 
 int sh_uniform_points(sh_ctx* c, int dim, int64_t n, uint64_t seed, int64_t start, int layout, double* out,

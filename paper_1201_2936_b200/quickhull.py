@@ -283,25 +283,43 @@ def quickhull_2d(points: PointSet, tol: Tolerance = Tolerance()) -> HullResult:
 def order_hull_2d(vertices: PointSet) -> PointSet:
     """CCW boundary order of a convex vertex set, starting at the
     lexicographically smallest vertex (reference quickhull.py:449-461: angle
-    sort around the centroid, stable).  The angles and the sort run on the
-    GPU; the result equals the reference's order whenever no two vertices
-    share an angle from the centroid (always, for a strictly convex set)."""
+    sort around the centroid, stable), computed on the GPU (sh_order_hull_2d:
+    centroid, atan2 keys, stable radix sort, rotation).  The result equals
+    the reference's order whenever no two vertices share an angle from the
+    centroid (always, for a strictly convex set)."""
     if vertices.dim != 2:
         raise ContractViolation("order_hull_2d needs 2D points")
     if vertices.n < 3:
         return vertices
-    x, y = (torch.from_numpy(c).to(torch.device("cuda", torch.cuda.current_device()))
+    device = torch.cuda.current_device()
+    x, y = (torch.from_numpy(np.ascontiguousarray(c)).to(torch.device("cuda", device))
             for c in vertices.coords)
-    ang = torch.atan2(y - y.mean(), x - x.mean())
-    order = torch.sort(ang, stable=True).indices
-    xs, ys = x[order], y[order]
-    # lexicographic minimum over (x, y, position), lowest position among ties
-    xmin = xs.min()
-    cand = torch.nonzero(xs == xmin).flatten()
-    ymin = ys[cand].min()
-    start = int(cand[ys[cand] == ymin][0])
-    xs, ys = torch.roll(xs, -start), torch.roll(ys, -start)
-    return PointSet((xs.cpu().numpy(), ys.cpu().numpy()))
+    perm = torch.empty(vertices.n, dtype=torch.int64, device=x.device)
+    with torch.cuda.device(device), _lib.device_lock(device):
+        rc = _lib.lib().sh_order_hull_2d(_lib.context(device), x.data_ptr(), y.data_ptr(), vertices.n,
+                                         perm.data_ptr(), _stream_ptr(device))
+    if rc != _lib.SH_OK:
+        _raise_for(rc)
+    p = perm.cpu().numpy()
+    return PointSet(tuple(np.ascontiguousarray(c[p]) for c in vertices.coords))
+
+
+def giftwrap_2d(points, eps: float):
+    """Indices of the strict 2D hull by gift wrapping on the device, in CCW
+    order from the lexicographic minimum (the reference's brute-force check,
+    hull2_giftwrap in the reference seghull/oracle module lines 20-52, used by the CLI's `verify`).  ``points``: (n, 2) float64
+    CUDA tensor."""
+    n = points.shape[0]
+    device = points.device.index
+    x, y = points[:, 0].contiguous(), points[:, 1].contiguous()
+    out = torch.empty(n + 1, dtype=torch.int64, device=points.device)
+    h = ctypes.c_int64(0)
+    with torch.cuda.device(device), _lib.device_lock(device):
+        rc = _lib.lib().sh_giftwrap_2d(_lib.context(device), x.data_ptr(), y.data_ptr(), n, float(eps),
+                                       out.data_ptr(), n + 1, ctypes.byref(h), _stream_ptr(device))
+    if rc != _lib.SH_OK:
+        _raise_for(rc)
+    return out[:h.value]
 
 
 def quickhull_3d(points: PointSet, tol: Tolerance = Tolerance(), facets: bool = False) -> HullResult:
