@@ -200,8 +200,11 @@ int64_t sh_launch_times(sh_ctx* ctx, int32_t* kind, float* ms, int64_t cap);
  * certified by the first query, support queries, points scanned, GJK
  * iterations, pruned by the local GJK, certified after the local GJK,
  * resolved by the global GJK, then SM cycles (summed over warps) spent in
- * the first query, the local GJK, the query after it and the global GJK.
- * Returns the count written (<= cap, <= 15). */
+ * the first query, the local GJK, the query after it and the global GJK;
+ * then (-DSH_FILTER_CYCLES builds) 20 log2 buckets of k_f_test's per-item
+ * wall cycles from 2^10 and the slowest item's cycles, GJK iterations,
+ * queries and scanned candidates.  Returns the count written (<= cap,
+ * <= 39). */
 int sh_filter_stats(sh_ctx* ctx, int64_t* out, int64_t cap);
 
 /* Diagnostics of the last 3D facet build: facets, queue items, wrap

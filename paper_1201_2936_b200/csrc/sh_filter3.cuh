@@ -64,6 +64,10 @@ struct FilterParams {
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
   unsigned long long local_in, local_out, fallback;
   unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;  // SM cycles per phase (summed over warps)
+  // -DSH_FILTER_CYCLES: k_f_test items by wall cycles (log2 buckets from
+  // 2^10), and the slowest item's cycles, GJK iterations, queries, scanned
+  uint32_t dur_hist[20];
+  unsigned long long dur_max, dur_max_iters, dur_max_queries, dur_max_scanned;
 };
 
 struct FilterWs {
@@ -191,6 +195,8 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
     P->local_out = 0;
     P->fallback = 0;
     P->cyc_cert = P->cyc_local = P->cyc_out = P->cyc_fallback = 0;
+    for (int k = 0; k < 20; k++) P->dur_hist[k] = 0;
+    P->dur_max = P->dur_max_iters = P->dur_max_queries = P->dur_max_scanned = 0;
     // box tree: level 0 = chunks of 32 candidates, level l+1 = 32 level-l nodes
     uint32_t nl = m ? (m + 31) / 32 : 0, off = 0, lev = 0;
     for (int l = 0; l < F_LEVELS; l++) {
@@ -1248,6 +1254,10 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
     if (lane == 0) j = atomicAdd(&f.fp->ctr_wl2, 1u);
     j = __shfl_sync(0xFFFFFFFFu, j, 0);
     if (j >= nwl2) break;
+#ifdef SH_FILTER_CYCLES
+    const long long t_item = clock64();
+    const unsigned long long it0 = fs.iters, q0 = fs.queries, sc0 = fs.scanned;
+#endif
     const uint32_t kk = f.wl2_k[j];
     const uint32_t k = kk & 0x7FFFFFFFu;
     const uint32_t ps = f.wl_ps[k];
@@ -1268,6 +1278,16 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
       f.keep[i] = (uint8_t)keep;
       amb_count += amb;
       cap_count += capped;
+#ifdef SH_FILTER_CYCLES
+      const unsigned long long dt = (unsigned long long)(clock64() - t_item);
+      int bkt = 63 - __clzll((long long)(dt | 1ull)) - 10;
+      atomicAdd(&f.fp->dur_hist[bkt < 0 ? 0 : (bkt > 19 ? 19 : bkt)], 1u);
+      if (dt > atomicMax(&f.fp->dur_max, dt)) {  // racy record of the slowest item (diagnostics)
+        f.fp->dur_max_iters = fs.iters - it0;
+        f.fp->dur_max_queries = fs.queries - q0;
+        f.fp->dur_max_scanned = fs.scanned - sc0;
+      }
+#endif
     }
   }
   if (lane == 0 && amb_count) atomicAdd(&f.fp->ambiguous, (uint32_t)amb_count);

@@ -1179,11 +1179,16 @@ int sh_filter_stats(sh_ctx* c, int64_t* out, int64_t cap) {
   if (!c || !c->fws.fp || cap <= 0) return 0;
   FilterParams P;
   if (cudaMemcpy(&P, c->fws.fp, sizeof(P), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
-  int64_t v[15] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
+  int64_t v[39] = {P.m, P.G, P.ambiguous, P.gjk_capped, (int64_t)P.certified, (int64_t)P.queries,
                    (int64_t)P.scanned, (int64_t)P.gjk_iters, (int64_t)P.local_in, (int64_t)P.local_out,
                    (int64_t)P.fallback, (int64_t)P.cyc_cert, (int64_t)P.cyc_local, (int64_t)P.cyc_out,
                    (int64_t)P.cyc_fallback};
-  int64_t n = std::min<int64_t>(cap, 15);
+  for (int k = 0; k < 20; k++) v[15 + k] = P.dur_hist[k];
+  v[35] = (int64_t)P.dur_max;
+  v[36] = (int64_t)P.dur_max_iters;
+  v[37] = (int64_t)P.dur_max_queries;
+  v[38] = (int64_t)P.dur_max_scanned;
+  int64_t n = std::min<int64_t>(cap, 39);
   for (int64_t i = 0; i < n; i++) out[i] = v[i];
   return (int)n;
 }

@@ -242,7 +242,8 @@ def hull_warnings(dim, res, trace_rows=None):
 
 FILTER_STATS = ("candidates", "grid", "ambiguous", "gjk_capped", "certified", "queries", "scanned",
                 "gjk_iters", "local_pruned", "local_extreme", "global_gjk", "cyc_cert", "cyc_local",
-                "cyc_query", "cyc_global")
+                "cyc_query", "cyc_global") + tuple(f"item_cyc_2^{10 + k}" for k in range(20)) + (
+                "item_cyc_max", "item_max_iters", "item_max_queries", "item_max_scanned")
 
 
 def filter_stats(device=None):
