@@ -942,6 +942,26 @@ __device__ __forceinline__ V3 f_cert_dir(V3 v, V3 ctr, double* len) {
   return w0;
 }
 
+// offsets of the 27 cells around a cell, nearest first: centre, 6 faces,
+// 12 edges, 8 corners
+__device__ __forceinline__ void f_nbr27(int t, int* dx, int* dy, int* dz) {
+  // code per neighbour: 2 bits per axis (0: -1, 1: 0, 2: +1)
+  constexpr unsigned char NB[27] = {0x15, 0x14, 0x16, 0x11, 0x19, 0x05, 0x25,              // centre, faces
+                                    0x10, 0x12, 0x18, 0x1a, 0x04, 0x06, 0x24, 0x26,        // edges (x,y) and (x,z)
+                                    0x01, 0x09, 0x21, 0x29,                                // edges (y,z)
+                                    0x00, 0x02, 0x08, 0x0a, 0x20, 0x22, 0x28, 0x2a};       // corners
+  const int c = NB[t];
+  *dx = (c & 3) - 1;
+  *dy = ((c >> 2) & 3) - 1;
+  *dz = ((c >> 4) & 3) - 1;
+}
+
+__device__ __forceinline__ uint32_t f_axis_cell_p(const FilterParams& P, int k, double x) {
+  const double t = (x - P.lo[k]) * P.inv_h[k];
+  const int c = (int)t;
+  return (uint32_t)(c < 0 ? 0 : (c >= (int)P.G ? (int)P.G - 1 : c));
+}
+
 // (1)-(3) for a candidate whose certificate query (k_f_cert) found the
 // candidate s0 above v's radial plane
 // mode 0: everything; mode 1: the first local GJK (k_f_local) already
@@ -961,12 +981,46 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   // all other candidates (a convex combination of them, so any simplex it
   // spans with candidates lies in their hull)
   if (MODE != 2) {
+    // the local set: the candidates of the 27 grid cells around v (centre
+    // cell, then faces, edges, corners), filled up with v's neighbours in
+    // Morton order; F_LOCAL * 32 points
     const uint32_t lo = ps > 16u * F_LOCAL ? ps - 16u * F_LOCAL : 0u;
+    uint32_t cstart = 0, ccnt = 0;
+    if (lane < 27) {
+      int dx, dy, dz;
+      f_nbr27((int)lane, &dx, &dy, &dz);
+      const int G = (int)P.G;
+      const int cx = (int)f_axis_cell_p(P, 0, v.x) + dx, cy = (int)f_axis_cell_p(P, 1, v.y) + dy,
+                cz = (int)f_axis_cell_p(P, 2, v.z) + dz;
+      if (cx >= 0 && cy >= 0 && cz >= 0 && cx < G && cy < G && cz < G) {
+        const uint32_t cell = spread3((uint32_t)cx) | (spread3((uint32_t)cy) << 1) | (spread3((uint32_t)cz) << 2);
+        cstart = __ldg(&f.cell_start[cell]);
+        ccnt = __ldg(&f.cell_start[cell + 1]) - cstart;
+      }
+    }
+    uint32_t incl = ccnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t ncell = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    const uint32_t excl = incl - ccnt;
     V3 lu[F_LOCAL];
     uint32_t lid[F_LOCAL];
 #pragma unroll
     for (int k = 0; k < F_LOCAL; k++) {
-      const uint32_t p = lo + k * 32 + lane;
+      const uint32_t slot = k * 32 + lane;
+      // the cell (lane) whose inclusive prefix first exceeds slot
+      uint32_t a = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t pv = __shfl_sync(0xFFFFFFFFu, incl, (int)(a + step - 1));
+        if (pv <= slot) a += step;
+      }
+      const uint32_t st0 = __shfl_sync(0xFFFFFFFFu, cstart, (int)(a & 31u));
+      const uint32_t ex0 = __shfl_sync(0xFFFFFFFFu, excl, (int)(a & 31u));
+      const uint32_t p = slot < ncell ? st0 + (slot - ex0) : lo + (slot - ncell);
       lid[k] = 0xFFFFFFFFu;
       lu[k] = v3(0.0, 0.0, 0.0);
       if (p < P.m && p != ps) {
