@@ -60,7 +60,7 @@ struct FilterParams {
   double gsum[3];              // sum of the candidates (deterministic order)
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
   uint32_t ambiguous, gjk_capped, nwl, ctr_wl;  // nwl: work-list length (k_f_cert)
-  uint32_t nwl2, ctr_wl2, pad2, pad3;            // second work list (k_f_local)
+  uint32_t nwl2, ctr_wl2, pad2, nparts;          // second work list (k_f_local); k_f_boxes01's blocks
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
   unsigned long long local_in, local_out, fallback;
   unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;  // SM cycles per phase (summed over warps)
@@ -310,66 +310,94 @@ __global__ void __launch_bounds__(BLOCK) k_f_count(Workspace ws, FilterWs f) {
 }
 
 // ------------------------------------------------------------------ F3
+// cell offsets: tiles of 8192 cells (1024 threads x 8 consecutive cells,
+// 16-byte loads; G^3 is a multiple of 8).  k_f_scan_tiles: each block the
+// total of its tile; k_f_scan: each block the exclusive scan of its tile
+// on top of the totals of the tiles before it.
+constexpr uint32_t F_SCAN_TILE = 8192;
+constexpr uint32_t F_SCAN_GRID = (uint32_t)FG_MAX * FG_MAX * FG_MAX / F_SCAN_TILE;
+
+__device__ __forceinline__ void f_load8(const uint32_t* a, uint32_t c, uint32_t cells, uint32_t* v) {
+  if (c < cells) {
+    const uint4 x = *reinterpret_cast<const uint4*>(a + c);
+    const uint4 y = *reinterpret_cast<const uint4*>(a + c + 4);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_f_scan_tiles(FilterWs f) {
+  __shared__ uint32_t s_w[32];
+  const uint32_t G = f.fp->G, cells = G * G * G;
+  const uint32_t base = blockIdx.x * F_SCAN_TILE;
+  if (base >= cells) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t v[8];
+  f_load8(f.cell_cnt, base + 8 * threadIdx.x, cells, v);
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) tot += v[k];
+  tot = __reduce_add_sync(0xFFFFFFFFu, tot);
+  if (lane == 0) s_w[warp] = tot;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = __reduce_add_sync(0xFFFFFFFFu, s_w[lane]);
+    if (lane == 0) f.wl_ps[blockIdx.x] = t;  // free until k_f_cert
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_f_scan(FilterWs f) {
-  // one block; tiles of 1024 x 8 cells, each thread 8 consecutive cells
-  // (two 16-byte loads, coalesced across the block; G^3 is a multiple of 8)
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
-  const uint32_t G = f.fp->G;
-  const uint32_t cells = G * G * G;
+  const uint32_t G = f.fp->G, cells = G * G * G;
+  const uint32_t base = blockIdx.x * F_SCAN_TILE;
+  if (base >= cells) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < cells; base += 8192) {
-    const uint32_t c = base + 8 * threadIdx.x;
-    uint32_t v[8];
-    if (c < cells) {
-      const uint4 a = *reinterpret_cast<const uint4*>(f.cell_cnt + c);
-      const uint4 b = *reinterpret_cast<const uint4*>(f.cell_cnt + c + 4);
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; k++) v[k] = 0;
-    }
-    uint32_t tot = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) tot += v[k];
-    uint32_t x = tot;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_w[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t w = s_w[lane];
-      uint32_t y = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
-        if (lane >= o) y += z;
-      }
-      s_w[lane] = y - w;
-    }
-    __syncthreads();
-    uint32_t run = s_carry + s_w[warp] + x - tot;
-    if (c < cells) {
-      uint32_t o[8];
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        o[k] = run;
-        run += v[k];
-      }
-      *reinterpret_cast<uint4*>(f.cell_start + c) = make_uint4(o[0], o[1], o[2], o[3]);
-      *reinterpret_cast<uint4*>(f.cell_start + c + 4) = make_uint4(o[4], o[5], o[6], o[7]);
-      *reinterpret_cast<uint4*>(f.cell_cur + c) = make_uint4(o[0], o[1], o[2], o[3]);
-      *reinterpret_cast<uint4*>(f.cell_cur + c + 4) = make_uint4(o[4], o[5], o[6], o[7]);
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = run;
-    __syncthreads();
+  if (warp == 0) {  // the tiles before this one
+    const uint32_t t = lane < blockIdx.x ? f.wl_ps[lane] : 0u;
+    const uint32_t c = __reduce_add_sync(0xFFFFFFFFu, t);
+    if (lane == 0) s_carry = c;
   }
-  if (threadIdx.x == 0) f.cell_start[cells] = s_carry;
+  const uint32_t c = base + 8 * threadIdx.x;
+  uint32_t v[8];
+  f_load8(f.cell_cnt, c, cells, v);
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) tot += v[k];
+  uint32_t x = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = s_w[lane];
+    uint32_t y = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
+      if (lane >= o) y += z;
+    }
+    s_w[lane] = y - w;
+  }
+  __syncthreads();
+  uint32_t run = s_carry + s_w[warp] + x - tot;
+  if (c < cells) {
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      o[k] = run;
+      run += v[k];
+    }
+    *reinterpret_cast<uint4*>(f.cell_start + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(f.cell_start + c + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    *reinterpret_cast<uint4*>(f.cell_cur + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(f.cell_cur + c + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    if (c + 8 == cells) f.cell_start[cells] = run;
+  }
 }
 
 // ------------------------------------------------------------------ F4
@@ -393,6 +421,31 @@ __global__ void __launch_bounds__(1024) k_f_boxes01(FilterWs f) {
   const FilterParams* P = f.fp;
   const uint32_t m = P->m, n0 = P->lnodes[0], n1 = P->lnodes[1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    // this block's part of the candidates' sum (discovery order, a fixed
+    // slice and reduction tree: deterministic), combined by k_f_boxes_hi
+    __shared__ double s_sum[32][3];
+    const uint32_t p0 = (uint32_t)(((uint64_t)m * blockIdx.x) / gridDim.x);
+    const uint32_t p1 = (uint32_t)(((uint64_t)m * (blockIdx.x + 1)) / gridDim.x);
+    double a[3] = {0.0, 0.0, 0.0};
+    for (uint32_t p = p0 + threadIdx.x; p < p1; p += 1024) {
+      a[0] += f.cx[p];
+      a[1] += f.cy[p];
+      a[2] += f.cz[p];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; k++)
+      for (int o = 16; o; o >>= 1) a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], o);
+    if (lane == 0)
+      for (int k = 0; k < 3; k++) s_sum[warp][k] = a[k];
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      double t = 0.0;
+      for (int w = 0; w < 32; w++) t += s_sum[w][threadIdx.x];
+      f.wl_val[3 * blockIdx.x + threadIdx.x] = t;  // free until k_f_cert
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.fp->nparts = gridDim.x;
+  }
   for (uint32_t base = blockIdx.x * 32; base < n0; base += gridDim.x * 32) {
     const uint32_t node = base + warp;
     double b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -445,30 +498,14 @@ __global__ void __launch_bounds__(1024) k_f_boxes01(FilterWs f) {
 }
 
 // levels 2.. (at most a few hundred nodes): one block, one warp per node;
-// the same block also sums the candidates in a fixed order (centroid)
+// the same block also adds up k_f_boxes01's partial sums in order (centroid)
 __global__ void __launch_bounds__(1024) k_f_boxes_hi(FilterWs f) {
   const FilterParams* P = f.fp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  {
-    __shared__ double s_sum[32][3];
-    double a[3] = {0.0, 0.0, 0.0};
-    for (uint32_t p = threadIdx.x; p < P->m; p += 1024) {
-      a[0] += f.cx[p];
-      a[1] += f.cy[p];
-      a[2] += f.cz[p];
-    }
-#pragma unroll
-    for (int k = 0; k < 3; k++)
-      for (int o = 16; o; o >>= 1) a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], o);
-    if (lane == 0)
-      for (int k = 0; k < 3; k++) s_sum[warp][k] = a[k];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t[3] = {0.0, 0.0, 0.0};
-      for (int w = 0; w < 32; w++)
-        for (int k = 0; k < 3; k++) t[k] += s_sum[w][k];
-      for (int k = 0; k < 3; k++) f.fp->gsum[k] = t[k];
-    }
+  if (threadIdx.x < 3) {  // the parts of k_f_boxes01, in order
+    double t = 0.0;
+    for (uint32_t b = 0; b < P->nparts; b++) t += f.wl_val[3 * b + threadIdx.x];
+    f.fp->gsum[threadIdx.x] = t;
   }
   for (int l = 2; l < (int)P->nlev; l++) {
     const uint32_t nl = P->lnodes[l], nc = P->lnodes[l - 1];
@@ -1238,7 +1275,7 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FCERT_MINB) k_f_cert(Workspac
 }
 
 #ifndef SH_FTEST_MINB
-#define SH_FTEST_MINB 2
+#define SH_FTEST_MINB 4
 #endif
 // the first local GJK for the work list of k_f_cert: pruned candidates are
 // settled here, the rest go to a second work list with the outcome
@@ -1360,37 +1397,80 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FTEST_MINB) k_f_test(Workspac
 }
 
 // ------------------------------------------------------------------ F6
-__global__ void __launch_bounds__(1024) k_f_compact(Workspace ws, FilterWs f) {
+// Kept candidates -> user indices in discovery order: each block of
+// k_f_ccount counts the kept ones of its slice; each block of k_f_compact
+// writes its slice at the total of the slices before it.
+constexpr uint32_t F_COMPACT_GRID = 128;
+
+__global__ void __launch_bounds__(1024) k_f_ccount(FilterWs f) {
   __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_carry;
+  const uint32_t m = f.fp->m;
+  const uint32_t p0 = (uint32_t)(((uint64_t)m * blockIdx.x) / gridDim.x);
+  const uint32_t p1 = (uint32_t)(((uint64_t)m * (blockIdx.x + 1)) / gridDim.x);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t c = 0;
+  for (uint32_t i = p0 + threadIdx.x; i < p1; i += 1024) c += f.keep[i] ? 1u : 0u;
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
+  if (lane == 0) s_w[warp] = c;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t t = __reduce_add_sync(0xFFFFFFFFu, s_w[lane]);
+    if (lane == 0) f.wl_pos[blockIdx.x] = t;  // free after k_f_test
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_f_compact(Workspace ws, FilterWs f) {
+  static_assert(F_COMPACT_GRID <= 1024, "one count per thread");
+  __shared__ uint32_t s_w[32], s_b[32], s_a[32];
+  __shared__ uint32_t s_carry, s_total;
   const uint32_t m = f.fp->m;
   int64_t* out = ws.st->out_idx;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < m; base += 1024) {
-    uint32_t i = base + threadIdx.x;
-    uint32_t v = (i < m && f.keep[i]) ? 1u : 0u;
-    uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
+  {  // kept candidates before this slice and in all slices
+    const uint32_t t = threadIdx.x < gridDim.x ? f.wl_pos[threadIdx.x] : 0u;
+    const uint32_t before = __reduce_add_sync(0xFFFFFFFFu, threadIdx.x < blockIdx.x ? t : 0u);
+    const uint32_t all = __reduce_add_sync(0xFFFFFFFFu, t);
+    if (lane == 0) {
+      s_b[warp] = before;
+      s_a[warp] = all;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t b2 = __reduce_add_sync(0xFFFFFFFFu, s_b[lane]);
+      const uint32_t a2 = __reduce_add_sync(0xFFFFFFFFu, s_a[lane]);
+      if (lane == 0) {
+        s_carry = b2;
+        s_total = a2;
+      }
+    }
+    __syncthreads();
+  }
+  const uint32_t p0 = (uint32_t)(((uint64_t)m * blockIdx.x) / gridDim.x);
+  const uint32_t p1 = (uint32_t)(((uint64_t)m * (blockIdx.x + 1)) / gridDim.x);
+  for (uint32_t base = p0; base < p1; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = (i < p1 && f.keep[i]) ? 1u : 0u;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v);
     if (lane == 0) s_w[warp] = __popc(bal);
     __syncthreads();
     if (warp == 0) {
-      uint32_t w = s_w[lane], y = w;
+      const uint32_t w = s_w[lane];
+      uint32_t y = w;
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
+        const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
         if (lane >= o) y += z;
       }
       s_w[lane] = y - w;
     }
     __syncthreads();
-    uint32_t pos = s_carry + s_w[warp] + __popc(bal & lanemask_lt());
+    const uint32_t pos = s_carry + s_w[warp] + __popc(bal & lanemask_lt());
     if (v) out[pos] = (int64_t)ws.vout[i];
     __syncthreads();
     if (threadIdx.x == 1023) s_carry = pos + v;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    f.result[0] = s_carry;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    f.result[0] = s_total;
     f.result[1] = 0;
     f.result[2] = 1;
     f.result[3] = f.fp->ambiguous;
@@ -1403,7 +1483,8 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_setup<<<grid, BLOCK, 0, s>>>(ws, f);
   k_f_gather<<<grid, BLOCK, 0, s>>>(ws, f);
   k_f_count<<<grid, BLOCK, 0, s>>>(ws, f);
-  k_f_scan<<<1, 1024, 0, s>>>(f);
+  k_f_scan_tiles<<<F_SCAN_GRID, 1024, 0, s>>>(f);
+  k_f_scan<<<F_SCAN_GRID, 1024, 0, s>>>(f);
   k_f_scatter<<<grid, BLOCK, 0, s>>>(f);
   k_f_boxes01<<<nsm * 2, 1024, 0, s>>>(f);
   k_f_boxes_hi<<<1, 1024, 0, s>>>(f);
@@ -1411,7 +1492,8 @@ static inline int filter_launch(FilterWs& f, Workspace ws, int nsm, cudaStream_t
   k_f_cert<<<nsm * 16, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_local<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
   k_f_test<<<nsm * 8, F_TEST_BLOCK, 0, s>>>(ws, f);
-  k_f_compact<<<1, 1024, 0, s>>>(ws, f);
+  k_f_ccount<<<F_COMPACT_GRID, 1024, 0, s>>>(f);
+  k_f_compact<<<F_COMPACT_GRID, 1024, 0, s>>>(ws, f);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : 10;
 }
 
