@@ -211,15 +211,22 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   r.mn.idx = 0xFFFFFFFFu;
   r.mx.idx = 0;
   r.mn.pad = r.mx.pad = 0;
+  // geometry.py:38-40, coordinates must be finite: NaN is caught here, an
+  // infinity by the reduced box (below)
+  bool nan_seen = false;
   auto visit = [&](const LexRec& q) {
+    // x range = the lexicographic extremes' x (set after the loops); only a
+    // point at or beyond them can replace them
 #pragma unroll
     for (int k = 0; k < DIM; k++) {
-      if (!isfinite(q.c[k])) st->nonfinite = 1;  // geometry.py:38-40: coordinates must be finite
-      r.lo[k] = fmin(r.lo[k], q.c[k]);
-      r.hi[k] = fmax(r.hi[k], q.c[k]);
+      nan_seen |= q.c[k] != q.c[k];
+      if (k > 0) {
+        r.lo[k] = fmin(r.lo[k], q.c[k]);
+        r.hi[k] = fmax(r.hi[k], q.c[k]);
+      }
     }
-    if (lex_less<DIM>(q, r.mn)) r.mn = q;
-    if (lex_less<DIM>(r.mx, q)) r.mx = q;
+    if (q.c[0] <= r.mn.c[0] && lex_less<DIM>(q, r.mn)) r.mn = q;
+    if (q.c[0] >= r.mx.c[0] && lex_less<DIM>(r.mx, q)) r.mx = q;
   };
   const uint32_t G = gridDim.x * BLOCK;
   uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
@@ -284,6 +291,11 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     q.pad = 0;
     visit(q);
   }
+  if (nan_seen) st->nonfinite = 1;
+  if (r.mn.idx != 0xFFFFFFFFu) {  // this thread saw a point
+    r.lo[0] = r.mn.c[0];
+    r.hi[0] = r.mx.c[0];
+  }
   // block reduce
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {
@@ -330,6 +342,9 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   }
   FirstRed t = s_w[0];
   st->ctr_red = 0;
+#pragma unroll
+  for (int k = 0; k < DIM; k++)
+    if (!isfinite(t.lo[k]) || !isfinite(t.hi[k])) st->nonfinite = 1;  // an infinity
   __threadfence();
   if (st->stats_out) {  // this slice's statistics (sh_hull_shard_begin)
     double* o = st->stats_out;
