@@ -919,7 +919,7 @@ struct SupU {
 };
 
 template <class SupFn>
-__device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters) {
+__device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters, int max_iters = 64) {
   V3 W[4];
   uint32_t id[4];
   int n = 1;
@@ -927,7 +927,7 @@ __device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters) {
   id[0] = first.id;
   V3 x = W[0];
 #pragma unroll 1
-  for (int it = 0; it < 64; it++) {
+  for (int it = 0; it < max_iters; it++) {
     const double xx = vdot(x, x);
     if (xx <= 0.0) return GJK_AMBIGUOUS;
     const V3 dir = vneg(x);
@@ -1210,7 +1210,9 @@ __device__ int f_decide(const FilterWs& f, const FilterParams& P, uint32_t ps, u
   first.u = vsub(v3(f.sx[s.pos], f.sy[s.pos], f.sz[s.pos]), v);
   V3 sep;
   iters = 0;
-  const int r = gjk(global_sup, first, eps, &sep, &iters);
+  // the last resort: a generous iteration cap (a capped GJK keeps the
+  // candidate, which is conservative; the tests assert it never happens)
+  const int r = gjk(global_sup, first, eps, &sep, &iters, 1024);
   fs.iters += iters;
   if (r == GJK_INSIDE) return 0;
   if (r == GJK_AMBIGUOUS) *amb = 1;

@@ -274,6 +274,30 @@ def _all_gather(t, group):
     return torch.stack(parts)
 
 
+def _single_rank(cols, offset, tol, return_info):
+    """hull_sharded on a one-rank group: the plain device hull, its indices
+    shifted by the slice offset; failures raise as from the protocol."""
+    from .quickhull import hull_indices_2d, hull_indices_3d
+    cols = _contiguous(cols)
+    dim, n = len(cols), cols[0].numel()
+    if n == 0:
+        idx, eps = torch.empty(0, dtype=torch.int64, device=cols[0].device), math.nan
+    else:
+        try:
+            if dim == 2:
+                idx, res = hull_indices_2d(cols, tol, return_info=True)
+            else:
+                idx, _, res = hull_indices_3d(cols, tol, return_info=True)
+        except DegenerateInputError:
+            raise
+        except Exception as e:
+            raise RuntimeError(f"sharded hull failed on rank(s) [0]: {e!r}") from e
+        idx, eps = idx + offset, float(res.eps)
+    if return_info:
+        return idx, {"eps": eps, "local_candidates": [idx.numel()], "union": idx.numel()}
+    return idx
+
+
 def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local_hull=None,
                  local_stats=None, reduce_stats=None, merge_hull=None, return_info=False):
     """Hull of a point cloud sharded over the ranks of ``group``.
@@ -288,6 +312,12 @@ def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local
     import torch.distributed as dist
     cols = _columns(points)
     dim = len(cols)
+    if (local_hull is None and local_stats is None and merge_hull is None
+            and dist.get_world_size(group) == 1):
+        # one rank: the slice is the whole input, so the global statistics
+        # are its own and the protocol reduces to the plain hull -- run that
+        # (no exchange, one graph launch)
+        return _single_rank(cols, offset, tol, return_info)
     staged = None
     if local_hull is None and local_stats is None:
         # the product path: the statistics come from the hull's own first pass
