@@ -153,4 +153,17 @@ SH_HD bool quotient_gt(double Db, double nb, double Da, double na) {
   return div_(Db, nb) > div_(Da, na);
 }
 
+#ifdef __CUDACC__
+// The same, with the (rare) division fallback taken by the warp only when
+// one of its lanes needs it: no per-lane divergence on the common path.
+__device__ __forceinline__ bool quotient_gt_warp(double Db, double nb, double Da, double na) {
+  const double p = mul(Db, na), r = mul(Da, nb);
+  const double diff = sub(p, r);
+  const bool sure = fabs(diff) > mul(1e-14, add(fabs(p), fabs(r)));
+  bool gt = diff > 0.0;
+  if (__any_sync(__activemask(), !sure)) gt = sure ? gt : (div_(Db, nb) > div_(Da, na));
+  return gt;
+}
+#endif
+
 }  // namespace sh

@@ -133,8 +133,8 @@ __device__ __forceinline__ int classify3(const Seg3& g, double qx, double qy, do
   // first argmax of D_j / |N_j| (np.argmax over the stacked quotients)
   int state = 0;
   double db = D0, nb = g.nrm[0];
-  if (quotient_gt(D1, g.nrm[1], db, nb)) { state = 1; db = D1; nb = g.nrm[1]; }
-  if (quotient_gt(D2, g.nrm[2], db, nb)) { state = 2; db = D2; }
+  if (quotient_gt_warp(D1, g.nrm[1], db, nb)) { state = 1; db = D1; nb = g.nrm[1]; }
+  if (quotient_gt_warp(D2, g.nrm[2], db, nb)) { state = 2; db = D2; }
   *dnext = db;
   return state;
 }

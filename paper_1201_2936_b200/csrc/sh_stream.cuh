@@ -133,12 +133,12 @@ __device__ __forceinline__ int cls3(const Seg3& g, double qx, double qy, double 
   const bool inside = (D0 <= g.thr[0]) & (D1 <= g.thr[1]) & (D2 <= g.thr[2]);
   int state = 0;
   double db = D0, nb = g.nrm[0];
-  if (quotient_gt(D1, g.nrm[1], db, nb)) {
+  if (quotient_gt_warp(D1, g.nrm[1], db, nb)) {
     state = 1;
     db = D1;
     nb = g.nrm[1];
   }
-  if (quotient_gt(D2, g.nrm[2], db, nb)) {
+  if (quotient_gt_warp(D2, g.nrm[2], db, nb)) {
     state = 2;
     db = D2;
   }
