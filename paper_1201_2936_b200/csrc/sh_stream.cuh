@@ -415,9 +415,10 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
   // classification of point i of a tile (the reference's fp64 order); returns
   // the child key (part * K + state) or 7 (dropped) and the child's distance
   auto classify_pt = [&](const StageDesc& d, const SegT* tab, uint32_t i, double x, double y, double z, uint32_t qi,
-                         double* dn) -> uint32_t {
+                         double* dn, auto one_tag) -> uint32_t {
+    constexpr bool ONE = decltype(one_tag)::value;  // the tile is one segment: one table for every point
     bool keep = i < d.count;
-    uint32_t part = (i >= d.bound) ? 1u : 0u;
+    uint32_t part = (!ONE && i >= d.bound) ? 1u : 0u;
     if (SRC == SRC_INPUT) {
       if (DIM == 2) {
         // quickhull.py:202-211: off the extreme line by more than eps
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
       uint32_t candmask = 0;
       // classification of the tile's points (TMA: from the stage; LDG: per-
       // point loads of the input, the fallback for non-unit strides)
-      auto classify = [&](auto tma_tag) {
+      auto classify = [&](auto tma_tag, auto one_tag) {
         constexpr bool TMA = decltype(tma_tag)::value;
 #pragma unroll
         for (int it = 0; it < IT; it++) {
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
             I[it] = d.base + i;
           }
           double dn;
-          uint32_t key = classify_pt(d, tab, i, X[it], Y[it], DIM == 3 ? Z[it] : 0.0, I[it], &dn);
+          uint32_t key = classify_pt(d, tab, i, X[it], Y[it], DIM == 3 ? Z[it] : 0.0, I[it], &dn, one_tag);
           if (SRC == SRC_INPUT && DIM == 3) {
             // the extreme points and the third corner are removed before the
             // split (quickhull.py:342)
@@ -535,8 +536,14 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
           nib += 1u << shf;
         }
       };
-      if (SRC == SRC_REC || d.mode == SM_TMA) classify(std::true_type{});
-      else classify(std::false_type{});
+      if (SRC == SRC_REC) {
+        if (d.bound == NONE) classify(std::true_type{}, std::true_type{});
+        else classify(std::true_type{}, std::false_type{});
+      } else if (d.mode == SM_TMA) {
+        classify(std::true_type{}, std::false_type{});
+      } else {
+        classify(std::false_type{}, std::false_type{});
+      }
       // ---- farthest-point candidates (rare after the first tiles): the
       // candidates are re-classified for their distances, then reduced per
       // child with REDUX (max distance bits, lowest original index)
@@ -548,7 +555,7 @@ __global__ void __launch_bounds__(StreamCfg<DIM>::NTHREADS, StreamCfg<DIM>::MINB
           cl[it] = 0;
           if ((candmask >> it) & 1u) {
             double dn;
-            classify_pt(d, tab, it * NT + tid, X[it], Y[it], DIM == 3 ? Z[it] : 0.0, I[it], &dn);
+            classify_pt(d, tab, it * NT + tid, X[it], Y[it], DIM == 3 ? Z[it] : 0.0, I[it], &dn, std::false_type{});
             cu[it] = (uint32_t)__double2hiint(dn) | 0x80000000u;
             cl[it] = (uint32_t)__double2loint(dn);
           }
