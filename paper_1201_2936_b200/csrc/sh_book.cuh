@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
   __shared__ RoundParams s_rp;
   __shared__ uint32_t s_seq;
   __shared__ Sum3 s_carry;
+  __shared__ uint32_t s_dead, s_status;  // final by now (the round kernel wrote them)
   // few children (flag written by the round kernel): block 0 does everything
   // in tile order with a running prefix -- no look-back, no arrival protocol
   const bool small = st->book_small != 0;
@@ -48,6 +49,8 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
   if (threadIdx.x == 0) {
     s_rp = st->rp;
     s_seq = st->seq;
+    s_dead = st->dead_round;
+    s_status = st->status;
     s_carry = s3_identity();
     if (!small) {
       __threadfence();
@@ -96,6 +99,8 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
     uint32_t cval[ITEMS3][4];
     // 3D child face (needed before the scan for the flat test)
     double fa[ITEMS3][3], fb[ITEMS3][3], fc[ITEMS3][3], fn[ITEMS3][3], fnl[ITEMS3];
+    // 2D child edge ends (loaded with the counts: one memory round trip)
+    double ea[ITEMS3][2], eb[ITEMS3][2];
 #pragma unroll
     for (int j = 0; j < ITEMS3; j++) {
       uint32_t e = base + j * BLOCK + tid;
@@ -103,10 +108,26 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
       v[j].idx = 0;
       v[j].cnt = 0;
       if (e < E) {
-        const uint32_t p = e / K;
-        v[j].cnt = __ldcg(&cur_in[e]) - __ldg(&par_start[p]);
+        const uint32_t p = e / K, s = e - p * K;
+        // count, farthest key and (2D) the parent's edge, all in flight at once
+        const uint32_t cin = __ldcg(&cur_in[e]), pst = __ldg(&par_start[p]);
+        const Key128 k = ld_cg(&ws.slot_key[e]);
+        if (DIM == 2) {
+          if (bp.root) {  // quickhull.py:217-222
+            ea[j][0] = (s == 0) ? st->pa[0] : st->pb[0];
+            ea[j][1] = (s == 0) ? st->pa[1] : st->pb[1];
+            eb[j][0] = (s == 0) ? st->pb[0] : st->pa[0];
+            eb[j][1] = (s == 0) ? st->pb[1] : st->pa[1];
+          } else {  // (a, far) / (far, b), quickhull.py:272-277
+            const Seg2& P = par2[p];
+            ea[j][0] = (s == 0) ? P.ax : P.fx;
+            ea[j][1] = (s == 0) ? P.ay : P.fy;
+            eb[j][0] = (s == 0) ? P.fx : P.bx;
+            eb[j][1] = (s == 0) ? P.fy : P.by;
+          }
+        }
+        v[j].cnt = cin - pst;
         if (v[j].cnt) {
-          Key128 k = ld_cg(&ws.slot_key[e]);
           v[j].hi = k.hi;
           v[j].idx = (uint32_t)k.lo;
           Key128 z;
@@ -224,19 +245,7 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
       F[1] = ld_coord(st->py, stride, far);
       F[2] = (DIM == 3) ? ld_coord(st->pz, stride, far) : 0.0;
       if (DIM == 2) {
-        double Ax, Ay, Bx, By;
-        if (bp.root) {  // quickhull.py:217-222
-          Ax = (s == 0) ? st->pa[0] : st->pb[0];
-          Ay = (s == 0) ? st->pa[1] : st->pb[1];
-          Bx = (s == 0) ? st->pb[0] : st->pa[0];
-          By = (s == 0) ? st->pb[1] : st->pa[1];
-        } else {        // (a, far) / (far, b), quickhull.py:272-277
-          const Seg2& P = par2[p];
-          Ax = (s == 0) ? P.ax : P.fx;
-          Ay = (s == 0) ? P.ay : P.fy;
-          Bx = (s == 0) ? P.fx : P.bx;
-          By = (s == 0) ? P.fy : P.by;
-        }
+        const double Ax = ea[j][0], Ay = ea[j][1], Bx = eb[j][0], By = eb[j][1];
         Seg2 g;
         g.ax = Ax; g.ay = Ay; g.bx = Bx; g.by = By; g.fx = F[0]; g.fy = F[1];
         // point_in_triangle(a, b, far): -eps * edge_length(.,.) per edge;
@@ -283,9 +292,9 @@ __global__ void __launch_bounds__(BLOCK, DIM == 2 ? 2 : 1) k_book(Workspace ws) 
       uint32_t nseg_next = T.v[0], n_next = T.v[1], emitted = T.v[2];
       // live points of the next round: records minus the DEAD padding the
       // round kernel claimed (quickhull.py's compact count)
-      const uint32_t n_true_next = T.v[3] - st->dead_round;
+      const uint32_t n_true_next = T.v[3] - s_dead;
       if (bp.root && nseg_next > 1) n_next += ws.slack;
-      uint32_t status = st->status;
+      uint32_t status = s_status;
       uint32_t round_next = bp.round + 1;  // the round the children belong to
       // every block has read this round's parameters before they change
       if (!small)

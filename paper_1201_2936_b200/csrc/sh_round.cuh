@@ -261,6 +261,14 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     }
     const uint32_t base = t * RTILE, end = min(base + (uint32_t)RTILE, n_live);
     const uint32_t lo = (t == t0) ? find_segment(base) : S.wnext[b ^ 1u];
+    // the first 32 segments' physical offsets and segment lo's table, in
+    // flight with the scan of their starts (one memory round trip)
+    using SegT0 = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
+    constexpr uint32_t TW = sizeof(SegT0) / 8;
+    static_assert(TW <= 32, "one table word per lane");
+    const unsigned long long phys0 = lo + lane < nseg ? seg_phys[lo + lane] : 0ull;
+    const unsigned long long tw0 =
+        lane < TW ? reinterpret_cast<const unsigned long long*>(ws.seg[cur])[(size_t)lo * TW + lane] : 0ull;
     uint32_t nw = 0, nxt = lo;
     for (uint32_t w0 = 0;; w0 += 32) {
       const uint32_t idx = lo + w0 + lane;
@@ -278,18 +286,14 @@ __global__ void __launch_bounds__(RB) k_round(Workspace ws) {
     }
     const bool slow = nw > (uint32_t)WMAX;
     if (!slow) {
-      for (uint32_t w = lane; w < nw; w += 32) S.wphys[b][w] = seg_phys[lo + w];
+      if (lane < nw) S.wphys[b][lane] = phys0;
+      for (uint32_t w = 32 + lane; w < nw; w += 32) S.wphys[b][w] = seg_phys[lo + w];
       __syncwarp();
       // one binary search per 32-point slot (all slots at once, one per lane)
       const uint32_t q = base + lane * 32;
       if (lane < RTILE / 32) S.wslot[b][lane] = q < n_live ? win_search(S.wstart[b], nw, q) : 0u;
     }
-    {
-      using SegT = typename std::conditional<DIM == 2, Seg2, Seg3>::type;
-      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ws.seg[cur]) +
-                                      (size_t)lo * (sizeof(SegT) / 8);
-      for (uint32_t k = lane; k < sizeof(SegT) / 8; k += 32) S.seg0[b][k] = src[k];
-    }
+    if (lane < TW) S.seg0[b][lane] = tw0;
     if (lane == 0) {
       S.wlo[b] = lo;
       S.wn[b] = nw;
