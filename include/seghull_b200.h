@@ -130,6 +130,14 @@ int sh_stats(sh_ctx* ctx, const double* x, const double* y, const double* z, int
 int sh_stats_reduce(sh_ctx* ctx, const double* gathered, int world, int dim, double* out, void* stream);
 int sh_set_shard(sh_ctx* ctx, const double* gstats, int64_t gidx_offset, int flags);
 
+/* Sharded merge of a 3D hull: the next sh_hull3d calls decide the extreme
+ * filter (quickhull.py:136-164) only for share `share` of `nshares` equal
+ * ranges of the candidates (in discovery order) and keep every
+ * other candidate.  The vertex lists of all shares, intersected, are the
+ * filtered hull (paper_1201_2936_b200/sharded.py splits the rank-0 merge's
+ * filter this way).  nshares = 1 restores the whole filter. */
+int sh_set_filter_share(sh_ctx* ctx, int share, int nshares);
+
 /* The same sharded hull in two halves around the exchange, without a
  * separate statistics pass: sh_hull_shard_begin launches the hull's own
  * first pass over the slice (bbox + lexicographic extremes), writes the

@@ -23,7 +23,7 @@ EXPORTED = ("sh_create", "sh_destroy", "sh_hull2d", "sh_hull3d", "sh_hull2d_asyn
             "sh_set_launch_mode", "sh_launch_times", "sh_filter_stats", "sh_bbox", "sh_segmented_scan", "sh_flag_permute",
             "sh_compact", "sh_scatter", "sh_orient_host", "sh_workspace_bytes", "sh_uniform_points", "sh_facet_stats",
             "sh_stats", "sh_stats_reduce", "sh_set_shard", "sh_hull_shard_begin", "sh_hull_shard_end",
-            "sh_order_hull_2d", "sh_giftwrap_2d",
+            "sh_order_hull_2d", "sh_giftwrap_2d", "sh_set_filter_share",
             "sh_last_error", "sh_version")
 SH_STATS, SH_SHARD_EPS, SH_SHARD_SPLIT = 14, 1, 2
 
@@ -115,6 +115,8 @@ def lib():
             L.sh_hull_shard_begin.restype = ctypes.c_int
             L.sh_hull_shard_end.argtypes = [P, P, ctypes.c_int, P, ctypes.POINTER(ShResult), P]
             L.sh_hull_shard_end.restype = ctypes.c_int
+            L.sh_set_filter_share.argtypes = [P, ctypes.c_int, ctypes.c_int]
+            L.sh_set_filter_share.restype = ctypes.c_int
             L.sh_order_hull_2d.argtypes = [P, P, P, I64, P, P]
             L.sh_order_hull_2d.restype = ctypes.c_int
             L.sh_giftwrap_2d.argtypes = [P, P, P, I64, D, P, I64, ctypes.POINTER(I64), P]

@@ -170,6 +170,7 @@ struct DevState {
   int64_t facet_cap;      // triples out_facets can hold
   uint32_t long_min_live; // k_stream long-round thresholds (long_round(); env overrides for tests)
   uint32_t long_seg_min;
+  uint32_t filter_share, filter_nshares;  // 3D filter decides only sorted candidates of share r of R (sh_set_filter_share)
   // sharded hulls (sh_set_shard): the all-ranks statistics (device, SH_STATS
   // doubles: -lo[3], hi[3], lex-min and lex-max records (x, y, z, global
   // index)), this slice's first global index, SHARD_* flags

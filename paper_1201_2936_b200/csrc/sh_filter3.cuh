@@ -61,6 +61,7 @@ struct FilterParams {
   unsigned long long bb[6];  // candidate bbox, ordered bits: min x,y,z then max x,y,z
   uint32_t ambiguous, gjk_capped, nwl, ctr_wl;  // nwl: work-list length (k_f_cert)
   uint32_t nwl2, ctr_wl2, pad2, nparts;          // second work list (k_f_local); k_f_boxes01's blocks
+  uint32_t share_lo, share_hi;                    // discovery indices this launch decides (the others are kept)
   unsigned long long queries, scanned, gjk_iters, certified;  // diagnostics
   unsigned long long local_in, local_out, fallback;
   unsigned long long cyc_cert, cyc_local, cyc_out, cyc_fallback;  // SM cycles per phase (summed over warps)
@@ -180,6 +181,13 @@ __global__ void __launch_bounds__(BLOCK) k_f_setup(Workspace ws, FilterWs f) {
     FilterParams* P = f.fp;
     P->m = m;
     P->G = G;
+    {  // sh_set_filter_share: a contiguous range of discovery indices (the
+       // Morton order within a grid cell depends on atomics, the discovery
+       // order does not: every launch of the merge sees the same partition)
+      const uint32_t R = st->filter_nshares > 1 ? st->filter_nshares : 1u, r = R > 1 ? st->filter_share : 0u;
+      P->share_lo = (uint32_t)(((uint64_t)m * r) / R);
+      P->share_hi = (uint32_t)(((uint64_t)m * (r + 1)) / R);
+    }
     P->ctr_test = 0;
     P->ambiguous = 0;
     P->gjk_capped = 0;
@@ -1244,7 +1252,7 @@ __global__ void __launch_bounds__(F_TEST_BLOCK, SH_FCERT_MINB) k_f_cert(Workspac
     ps = __shfl_sync(0xFFFFFFFFu, ps, 0);
     if (ps >= m) break;
     const uint32_t i = __ldg(&f.sid[ps]);
-    if (m <= 4) {  // quickhull.py:148-149
+    if (m <= 4 || i < P.share_lo || i >= P.share_hi) {  // quickhull.py:148-149; another share's
       if (lane == 0) f.keep[i] = 1;
       continue;
     }

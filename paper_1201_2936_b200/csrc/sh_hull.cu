@@ -89,6 +89,7 @@ struct sh_ctx {
   double* stage_stats = nullptr;  // stats_out of the current stage-1 launch
   int round_occ2 = 0, round_occ3 = 0, book_occ2 = 0, book_occ3 = 0;
   int stream_occ2 = 1, stream_occ3 = 1;  // k_stream blocks per SM
+  uint32_t filter_share = 0, filter_nshares = 1;  // sh_set_filter_share
   uint32_t last_n = 0;
   bool last_facets = false;
   int launch_mode = 0;  // 0: CUDA graph with device-side WHILE; 1: host loop; 2: host loop + events
@@ -511,6 +512,8 @@ static int hull_async(sh_ctx* c, const double* x, const double* y, const double*
     h->long_min_live = e1 ? (uint32_t)strtoul(e1, nullptr, 10) : LONG_MIN_LIVE;
     h->long_seg_min = e2 ? (uint32_t)strtoul(e2, nullptr, 10) : LONG_SEG_MIN;
   }
+  h->filter_share = c->filter_share;
+  h->filter_nshares = c->filter_nshares;
   h->gstats = c->shard_gstats;
   h->gidx_offset = c->shard_offset;
   h->shard_flags = c->shard_gstats ? c->shard_flags : 0u;
@@ -901,6 +904,14 @@ int sh_set_shard(sh_ctx* c, const double* gstats, int64_t gidx_offset, int flags
   c->shard_gstats = gstats;
   c->shard_offset = gidx_offset;
   c->shard_flags = (uint32_t)flags;
+  return SH_OK;
+}
+
+int sh_set_filter_share(sh_ctx* c, int share, int nshares) {
+  if (!c) return set_err(SH_CONTRACT, "null context");
+  if (nshares < 1 || share < 0 || share >= nshares) return set_err(SH_CONTRACT, "bad filter share");
+  c->filter_share = (uint32_t)share;
+  c->filter_nshares = (uint32_t)nshares;
   return SH_OK;
 }
 

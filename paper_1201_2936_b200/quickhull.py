@@ -141,6 +141,26 @@ class _Shard:
             _lib.lib().sh_set_shard(self.ctx, None, 0, 0)
 
 
+class _FilterShare:
+    """sh_set_filter_share for the duration of one 3D hull call: the filter
+    decides only share r of R of the candidates and keeps the others
+    (sharded.py's split merge)."""
+
+    def __init__(self, share, ctx):
+        self.share, self.ctx = share, ctx
+
+    def __enter__(self):
+        if self.share is not None:
+            r, R = self.share
+            rc = _lib.lib().sh_set_filter_share(self.ctx, int(r), int(R))
+            if rc != _lib.SH_OK:
+                _raise_for(rc)
+
+    def __exit__(self, *exc):
+        if self.share is not None:
+            _lib.lib().sh_set_filter_share(self.ctx, 0, 1)
+
+
 def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False, shard=None):
     """Original indices (int64 tensor) of the 2D hull vertices.
 
@@ -168,14 +188,17 @@ def hull_indices_2d(points, tol: Tolerance = Tolerance(), return_info=False, sha
     return (idx, res) if return_info else idx
 
 
-def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False, shard=None):
+def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_info=False, shard=None,
+                    filter_share=None):
     """Original indices (int64 tensor) of the 3D hull vertices, plus the
     (f, 3) int32 facet triples when ``facets`` is true: original indices,
     counter-clockwise seen from outside, exact (coplanar vertices are
     triangulated consistently), order unspecified.  Host input is handled
-    like in hull_indices_2d."""
+    like in hull_indices_2d.  ``filter_share`` (r, R): the extreme filter
+    decides only share r of R of the candidates and keeps the rest (the
+    intersection over the R shares is the hull)."""
     if _on_host(points):
-        r = hull_indices_3d(_to_cuda(points), tol, facets, return_info)
+        r = hull_indices_3d(_to_cuda(points), tol, facets, return_info, shard, filter_share)
         if return_info:
             return r[0].cpu(), (None if r[1] is None else r[1].cpu()), r[2]
         return (r[0].cpu(), None if r[1] is None else r[1].cpu()) if facets else r.cpu()
@@ -192,7 +215,7 @@ def hull_indices_3d(points, tol: Tolerance = Tolerance(), facets=False, return_i
         with torch.cuda.device(device), _lib.device_lock(device):
             ctx = _lib.context(device)
             out = _out_buffer(device, n)
-            with _Shard(shard, ctx):
+            with _Shard(shard, ctx), _FilterShare(filter_share, ctx):
                 rc = _lib.lib().sh_hull3d(ctx, ptrs[0], ptrs[1], ptrs[2], stride, n, tol.eps_rel,
                                           tol.eps_abs, out.data_ptr(),
                                           fout.data_ptr() if facets else None, fcap,

@@ -221,12 +221,16 @@ def _globalize(cols, offset, idx, gstats):
     return gidx, coords
 
 
-def device_merge_hull(cols, tol: Tolerance):
-    """The rank-0 hull of the union (plain hull: the union holds the global
-    extremes as real points; tol carries the global eps)."""
+def device_merge_hull(cols, tol: Tolerance, share=None):
+    """The hull of the union (plain hull: the union holds the global extremes
+    as real points; tol carries the global eps).  share (r, R): in 3D the
+    extreme filter decides only share r of R of the candidates and keeps the
+    others (the split merge of hull_sharded)."""
     from .quickhull import hull_indices_2d, hull_indices_3d
     cols = _contiguous(cols)
-    return hull_indices_2d(cols, tol) if len(cols) == 2 else hull_indices_3d(cols, tol)
+    if len(cols) == 2:
+        return hull_indices_2d(cols, tol)
+    return hull_indices_3d(cols, tol, filter_share=share)
 
 
 def _local(cols, offset, tol, gstats, local_hull, device):
@@ -247,9 +251,9 @@ def _local(cols, offset, tol, gstats, local_hull, device):
         return torch.zeros((0, dim + 1), dtype=torch.float64, device=device), 2, math.nan, repr(e)
 
 
-def _merge(union, dim, eps, merge_hull):
+def _merge(union, dim, eps, merge_hull, share=None):
     """Final hull of the gathered records (deduplicated, in global index
-    order); returns global indices."""
+    order); returns global indices.  share: see device_merge_hull."""
     if union.shape[0] == 0:
         return torch.empty(0, dtype=torch.int64, device=union.device)
     union = union[torch.argsort(union[:, dim])]
@@ -257,7 +261,8 @@ def _merge(union, dim, eps, merge_hull):
     keep[1:] = union[1:, dim] != union[:-1, dim]  # a global extreme comes from every slice
     union = union[keep]
     cols = tuple(union[:, k].contiguous() for k in range(dim))
-    idx = merge_hull(cols, Tolerance(eps_abs=eps))
+    t = Tolerance(eps_abs=eps)
+    idx = merge_hull(cols, t) if share is None else merge_hull(cols, t, share=share)
     return union[idx.to(union.device), dim].to(torch.int64)
 
 
@@ -299,7 +304,8 @@ def _single_rank(cols, offset, tol, return_info):
 
 
 def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local_hull=None,
-                 local_stats=None, reduce_stats=None, merge_hull=None, return_info=False):
+                 local_stats=None, reduce_stats=None, merge_hull=None, return_info=False,
+                 split_merge=None):
     """Hull of a point cloud sharded over the ranks of ``group``.
 
     points: this rank's slice, an (n_i, dim) float64 tensor or a tuple of dim
@@ -307,7 +313,10 @@ def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local
     stand-ins ``local_hull``, ``local_stats``, ``reduce_stats`` and
     ``merge_hull`` are given).  offset: global index of the slice's first
     point.  Returns the global vertex indices (int64) on rank 0 and None on
-    the other ranks; every rank raises if any rank failed.
+    the other ranks; every rank raises if any rank failed.  split_merge (3D;
+    default: on for the product path): every rank runs the merge loop on the
+    gathered union and decides the extreme filter for its share of the
+    candidates; rank 0 intersects the vertex lists (one more all-gather).
     """
     import torch.distributed as dist
     cols = _columns(points)
@@ -370,22 +379,41 @@ def hull_sharded(points, offset, tol: Tolerance = Tolerance(), group=None, local
     pad = torch.zeros((cap, dim + 1), dtype=torch.float64, device=dev)
     pad[:rec.shape[0]] = rec
     parts = _all_gather(pad, group)
-    # 4. rank 0: hull of the union
+    # 4. hull of the union: on rank 0, or (3D, split) the loop on every rank
+    # with the filter split over the ranks, the vertex lists intersected
+    if split_merge is None:
+        split_merge = merge_hull is device_merge_hull
+    split = split_merge and dim == 3
     result = None
-    if rank == 0:
+    if rank == 0 or split:
         if math.isnan(eps):
             eps = eps_of_stats(gstats, dim, tol)
         union = torch.cat([parts[r, :c] for r, c in enumerate(counts)], dim=0)
-        result = _merge(union, dim, eps, merge_hull)
+        if not split:
+            result = _merge(union, dim, eps, merge_hull)
+        else:
+            mine = _merge(union, dim, eps, merge_hull, share=(rank, world))
+            lens = _all_gather(torch.tensor([mine.numel()], dtype=torch.int64, device=dev), group)
+            lens = lens.view(-1).cpu().tolist()
+            padk = torch.full((max(max(lens), 1),), -1, dtype=torch.int64, device=dev)
+            padk[:mine.numel()] = mine.to(dev)
+            allk = _all_gather(padk, group)
+            if rank == 0:
+                keep = torch.ones(mine.numel(), dtype=torch.bool, device=dev)
+                for r in range(1, world):
+                    keep &= torch.isin(padk[:mine.numel()], allk[r, :lens[r]])
+                result = mine.to(dev)[keep]
     if return_info:
         return result, {"eps": eps, "local_candidates": counts, "union": sum(counts)}
     return result
 
 
 def hull_sharded_loopback(points, nshards, tol: Tolerance = Tolerance(), local_hull=None,
-                          local_stats=None, reduce_stats=None, merge_hull=None, return_info=False):
+                          local_stats=None, reduce_stats=None, merge_hull=None, return_info=False,
+                          split_merge=None):
     """The same shard -> merge pipeline for ``nshards`` contiguous slices in
-    one process (collectives replaced by their obvious local equivalents)."""
+    one process (collectives replaced by their obvious local equivalents;
+    the split 3D merge runs its shares one after the other)."""
     cols = _columns(points)
     dim = len(cols)
     n = cols[0].numel()
@@ -409,7 +437,16 @@ def hull_sharded_loopback(points, nshards, tol: Tolerance = Tolerance(), local_h
     if math.isnan(eps):
         eps = eps_of_stats(gstats, dim, tol)
     union = torch.cat(recs, dim=0)
-    result = _merge(union, dim, eps, merge_hull)
+    if split_merge is None:
+        split_merge = merge_hull is device_merge_hull
+    if split_merge and dim == 3 and nshards > 1:
+        lists = [_merge(union, dim, eps, merge_hull, share=(r, nshards)) for r in range(nshards)]
+        keep = torch.ones(lists[0].numel(), dtype=torch.bool, device=lists[0].device)
+        for other in lists[1:]:
+            keep &= torch.isin(lists[0], other)
+        result = lists[0][keep]
+    else:
+        result = _merge(union, dim, eps, merge_hull)
     if return_info:
         return result, {"eps": eps, "local_candidates": [r.shape[0] for r in recs], "union": union.shape[0]}
     return result

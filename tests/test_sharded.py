@@ -84,6 +84,53 @@ def cpu_merge(cols, tol):
 CPU = dict(local_hull=cpu_hull, local_stats=cpu_stats, reduce_stats=cpu_reduce_stats, merge_hull=cpu_merge)
 
 
+def cpu_merge_share(cols, tol, share=None):
+    """Stand-in for the split merge (3D): share r of R returns the hull plus
+    the union points whose position is not congruent to r mod R -- like the
+    device filter, which keeps every candidate outside its share; only the
+    intersection over the shares is the hull."""
+    exact = cpu_merge(cols, tol)
+    if share is None:
+        return exact
+    r, R = share
+    n = cols[0].numel()
+    extra = torch.tensor([p for p in range(n) if p % R != r], dtype=torch.int64)
+    extra = extra[~torch.isin(extra, exact)]
+    return torch.cat([exact, extra])
+
+
+def _split_worker(rank, world, port, kind, n, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    cols = generate(kind, n, 0)
+    b = [(n * r) // world for r in range(world + 1)]
+    mine = tuple(torch.from_numpy(np.ascontiguousarray(c[b[rank]:b[rank + 1]])) for c in cols)
+    hooks = dict(CPU, merge_hull=cpu_merge_share)
+    res = sharded.hull_sharded(mine, b[rank], Tolerance(), split_merge=True, **hooks)
+    q.put((rank, None if res is None else np.sort(res.numpy())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_split_merge_intersects_shares(world):
+    """3D merge split over the ranks (every rank runs the merge with its
+    filter share, rank 0 intersects): the whole input's hull on rank 0."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, "uniform-ball", 30_000, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(out[r] is None for r in range(1, world))
+    assert np.array_equal(out[0], whole(generate("uniform-ball", 30_000, 0)))
+
+
 def whole(cols):
     if len(cols) == 2:
         return np.sort(oracle.hull2d(*cols).idx)
@@ -222,6 +269,52 @@ def test_loopback_gpu_matches_single(kind, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kind,n", [("uniform-ball", 2_000_000), ("unit-cube", 1_000_000)])
+def test_split_filter_shares_intersect_to_the_hull(kind, n):
+    """sh_set_filter_share: every share keeps a superset of the hull, the
+    candidates outside the share included; the intersection is the hull."""
+    import paper_1201_2936_b200 as P
+    cols = generate(kind, n, 0)
+    d = tuple(torch.from_numpy(c).cuda() for c in cols)
+    full = P.hull_indices_3d(d)
+    for R in (2, 5):
+        parts = [P.hull_indices_3d(d, filter_share=(r, R)) for r in range(R)]
+        for p in parts:
+            assert torch.isin(full, p).all()
+        keep = torch.ones(parts[0].numel(), dtype=torch.bool, device=parts[0].device)
+        for p in parts[1:]:
+            keep &= torch.isin(parts[0], p)
+        assert torch.equal(parts[0][keep], full)  # discovery order kept
+    assert torch.equal(P.hull_indices_3d(d), full)  # the setting does not persist
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n", [("uniform-ball", 2_000_000), ("uniform-disk", 2_000_000)])
+def test_staged_ranks_emulated_on_one_gpu(kind, n):
+    """The product path's two-stage slice hull (sh_hull_shard_begin / _end)
+    for two slices in turn, with the statistics of the other slice from
+    sh_stats, then the (split) merge: equal to the single hull."""
+    cols = generate(kind, n, 0)
+    d = tuple(torch.from_numpy(c).cuda() for c in cols)
+    dim = len(cols)
+    b = [0, n // 3, n]
+    slices = [tuple(c[b[r]:b[r + 1]].contiguous() for c in d) for r in range(2)]
+    recs = []
+    for r in range(2):
+        staged = sharded.StagedDeviceHull()
+        st = staged.begin(slices[r], b[r], Tolerance())
+        other = sharded.device_stats(slices[1 - r], b[1 - r])
+        gstats = sharded.device_reduce_stats(torch.stack([st, other] if r == 0 else [other, st]), dim)
+        gidx, coords, eps = staged.end(slices[r], b[r], Tolerance(), gstats)
+        recs.append(torch.cat([coords, gidx.to(torch.float64)[:, None]], dim=1))
+    union = torch.cat(recs)
+    split = [sharded._merge(union, dim, eps, sharded.device_merge_hull, share=(r, 2) if dim == 3 else None)
+             for r in range(2)]
+    got = split[0][torch.isin(split[0], split[1])]
+    assert np.array_equal(np.sort(got.cpu().numpy()), whole(cols))
+
+
+@pytest.mark.gpu
 def test_device_bbox_matches_numpy():
     cols = generate("uniform-ball", 1_000_001, 3)
     bb = sharded.device_bbox(tuple(torch.from_numpy(c).cuda() for c in cols)).cpu().numpy()
@@ -279,8 +372,8 @@ def test_nccl_world2_matches_single(kind, n):
 @pytest.mark.parametrize("kind,n", [("uniform-disk", 3_000_000), ("uniform-ball", 1_000_000),
                                     ("unit-cube", 200_000), ("near-circle", 500_000)])
 def test_nccl_world1_staged_matches_single(kind, n):
-    """The product path (hull in two stages around the NCCL exchange) on a
-    one-rank communicator: equal to the single hull."""
+    """The product path on a one-rank communicator (the plain hull, no
+    exchange): equal to the single hull."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
