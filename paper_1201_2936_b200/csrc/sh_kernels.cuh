@@ -194,10 +194,20 @@ __device__ void finish_first_reduce(Workspace ws, FirstRed t) {
   }
 }
 
+// Blocks a pass over the input uses: the whole grid for large inputs, fewer
+// for small ones (>= 32 points per thread), so the per-block reductions,
+// partials and atomics do not dominate a short pass.
+__device__ __forceinline__ uint32_t first_pass_blocks(uint32_t n) {
+  const uint32_t want = (uint32_t)(((uint64_t)n + BLOCK * 32u - 1) / (BLOCK * 32u));
+  return want < 1u ? 1u : (want < gridDim.x ? want : gridDim.x);
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
   DevState* st = ws.st;
   const uint32_t n = st->n;
+  const uint32_t nb = first_pass_blocks(n);
+  if (blockIdx.x >= nb) return;
   const int64_t stride = st->stride;
   const double* P[3] = {st->px, st->py, st->pz};
   FirstRed r;
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     if (q.c[0] <= r.mn.c[0] && lex_less<DIM>(q, r.mn)) r.mn = q;
     if (q.c[0] >= r.mx.c[0] && lex_less<DIM>(r.mx, q)) r.mx = q;
   };
-  const uint32_t G = gridDim.x * BLOCK;
+  const uint32_t G = nb * BLOCK;
   uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
   bool aligned = stride == 1;
 #pragma unroll
@@ -313,7 +323,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     parts[blockIdx.x] = s_w[0];
     __threadfence();
     uint32_t done = atomicAdd(&st->ctr_red, 1u);
-    s_last = (done == gridDim.x - 1);
+    s_last = (done == nb - 1);
   }
   __syncthreads();
   if (!s_last) return;
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_reduce(Workspace ws) {
     const FirstRed* parts = reinterpret_cast<const FirstRed*>(ws.red);
     FirstRed t = r;
     bool any = false;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+    for (uint32_t b = threadIdx.x; b < nb; b += BLOCK) {
       FirstRed o = ld_cg_fr(parts + b);
       if (!any) t = o;
       else fr_merge<DIM>(t, o);
@@ -410,6 +420,8 @@ __global__ void __launch_bounds__(BLOCK) k_first_count(Workspace ws) {
   DevState* st = ws.st;
   const RoundParams rp = st->rp;
   if (!rp.active || !rp.root) return;
+  const uint32_t nb = first_pass_blocks(st->n);
+  if (blockIdx.x >= nb) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->ctr_book = 0;
     st->arrive_book = 0;
@@ -457,7 +469,7 @@ __global__ void __launch_bounds__(BLOCK) k_first_count(Workspace ws) {
   bool aligned = stride == 1;
 #pragma unroll
   for (int k = 0; k < DIM; k++) aligned = aligned && ((reinterpret_cast<uintptr_t>(P[k]) & 15) == 0);
-  const uint32_t G = gridDim.x * BLOCK;
+  const uint32_t G = nb * BLOCK;
   uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
   if (aligned) {
     const uint32_t npair = n / 2;
@@ -688,6 +700,8 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
   DevState* st = ws.st;
   if (st->first_active != 2) return;
   const uint32_t n = st->n;
+  const uint32_t nb = first_pass_blocks(n);
+  if (blockIdx.x >= nb) return;
   const int64_t stride = st->stride;
   const double pa0 = st->pa[0], pa1 = st->pa[1], pa2 = st->pa[2];
   const double ux = sub(st->pb[0], pa0), uy = sub(st->pb[1], pa1), uz = sub(st->pb[2], pa2);
@@ -708,7 +722,7 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
     k.pad = 0;
     if (ki_better(k, best)) best = k;
   };
-  const uint32_t G = gridDim.x * BLOCK;
+  const uint32_t G = nb * BLOCK;
   uint32_t i = blockIdx.x * BLOCK + threadIdx.x;
   for (; (uint64_t)i + 3ull * G < n; i += 4 * G) {
     double x[4], y[4], z[4];
@@ -740,7 +754,7 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
     parts[blockIdx.x] = s_w[0];
     __threadfence();
     uint32_t done = atomicAdd(&st->ctr_red, 1u);
-    s_last = (done == gridDim.x - 1);
+    s_last = (done == nb - 1);
   }
   __syncthreads();
   if (!s_last) return;
@@ -751,7 +765,7 @@ __global__ void __launch_bounds__(BLOCK) k_line_far(Workspace ws) {
     t.hi = 0;
     t.idx = 0xFFFFFFFFu;
     t.pad = 0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += BLOCK) {
+    for (uint32_t b = threadIdx.x; b < nb; b += BLOCK) {
       KeyIdx o;
       o.hi = __ldcg(&parts[b].hi);
       o.idx = __ldcg(&parts[b].idx);
