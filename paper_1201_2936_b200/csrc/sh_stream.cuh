@@ -68,10 +68,10 @@ constexpr int SRC_REC = 1;    // rounds >= 2: the live records of the previous r
 #define SH_S3_NW 7
 #endif
 #ifndef SH_S3_IT
-#define SH_S3_IT 4
+#define SH_S3_IT 5
 #endif
 #ifndef SH_S3_S
-#define SH_S3_S 4
+#define SH_S3_S 3
 #endif
 
 template <int DIM>
