@@ -53,10 +53,10 @@ constexpr int SRC_REC = 1;    // rounds >= 2: the live records of the previous r
 #define SH_S2_NW 7
 #endif
 #ifndef SH_S2_IT
-#define SH_S2_IT 6
+#define SH_S2_IT 8
 #endif
 #ifndef SH_S2_S
-#define SH_S2_S 4
+#define SH_S2_S 3
 #endif
 #ifndef SH_S2_MINB
 #define SH_S2_MINB 2
