@@ -965,7 +965,7 @@ __device__ int gjk(SupFn&& sup, SupU first, double eps, V3* sep, int* iters, int
 }
 
 #ifndef F_LOCAL_N
-#define F_LOCAL_N 6
+#define F_LOCAL_N 4
 #endif
 constexpr int F_LOCAL = F_LOCAL_N;
 #ifndef SH_F_EXTRA
