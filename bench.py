@@ -308,10 +308,13 @@ def run_sharded(args, ws, rank, local):
                                     tot_ms / args.steps)
     launches = None
     if roofline:
-        # per rank and step: stats + stats reduction, the local hull (as in
-        # main()), rank 0's merge hull of the gathered candidates (not counted)
+        # per rank and step: the local hull's graph (as in main(); with more
+        # than one rank also stage 1 / 2 and the statistics reduction), rank
+        # 0's merge hull of the gathered candidates not counted
         r = roofline["launches"] - 1
-        launches = args.steps * (2 + 4 + 2 * r + min(3, max(0, r - 1)) + (12 if dim == 3 else 0))
+        long_peel = 5
+        launches = args.steps * ((2 if ws > 1 else 0) + 4 + (1 if dim == 3 else 0) + 2 + 3 * long_peel
+                                 + 2 * max(0, r - 1 - long_peel) + (14 if dim == 3 else 1))
     if rank == 0:
         h = int(res.numel())
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
@@ -508,13 +511,15 @@ def main():
     assert L.sh_fetch(ctx, ctypes.byref(res), sp) == 0
     assert int(res.h) == h and int(res.iterations) == rounds
     value = n * ws * args.steps / (tot_ms / 1e3) / 1e6
-    # init, first reduce, first-split count, book, then (round, book) per
-    # round, then output (2D) or line-far + 9 filter kernels (3D)
-    # + one unused launch per peeled round (k_round_long / k_round pair,
-    # rounds 2..4 outside the WHILE node); 3D: line-far + 12 filter kernels
-    # instead of k_output; facets: 9 kernels
-    peeled = max(0, min(3, rounds - 1))
-    launches_per_hull = 5 + 2 * rounds + peeled + (12 if dim == 3 else 0) + (9 if want_fac else 0)
+    # the hull graph's kernel launches: init, first reduce, [3D: line-far],
+    # first-split count, its book; round 1 (k_stream) and its book; LONG_PEEL
+    # peeled round bodies outside the WHILE node, each (k_stream, k_round,
+    # k_book) whether or not rounds are left (csrc/sh_common.cuh
+    # SH_LONG_PEEL); (k_round, k_book) per WHILE iteration; then k_output
+    # (2D) or the 14 filter kernels (3D); facets: 9 kernels
+    long_peel = 5
+    launches_per_hull = (4 + (1 if dim == 3 else 0) + 2 + 3 * long_peel + 2 * max(0, rounds - 1 - long_peel)
+                         + (14 if dim == 3 else 1) + (9 if want_fac else 0))
 
     # ---------------- per-kernel pass (events after every launch)
     roofline = measure_roofline(L, ctx, local, launch, n, dim, args.config, tot_ms / args.steps)

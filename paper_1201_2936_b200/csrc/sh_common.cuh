@@ -254,7 +254,10 @@ struct Workspace {
 // node only k_round runs, so the later, short rounds pay no extra launch.
 constexpr uint32_t LONG_SEG_MIN = 4096;
 constexpr uint32_t LONG_MIN_LIVE = 4u << 20;
-constexpr int LONG_PEEL = 3;  // rounds 2..4 are launched outside the WHILE loop
+#ifndef SH_LONG_PEEL
+#define SH_LONG_PEEL 5
+#endif
+constexpr int LONG_PEEL = SH_LONG_PEEL;  // rounds 2..6 are launched outside the WHILE loop
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ unsigned long long pow2_dev(unsigned long long x) {

@@ -1,7 +1,7 @@
 """GPU: the streaming long-segment round kernel (k_round_long,
-csrc/sh_round1.cuh) on every peeled round, including its point-by-point
+csrc/sh_stream.cuh) on every peeled round, including its point-by-point
 path for chunks that overlap three or more segments: the thresholds are
-lowered through SH_LONG_MIN_LIVE / SH_LONG_SEG_MIN so that rounds 2-4 of
+lowered through SH_LONG_MIN_LIVE / SH_LONG_SEG_MIN so that rounds 2-6 of
 small and fragmented inputs all take it.  Bar: identical vertex lists
 (discovery order in 2D), iterations and per-round traces vs the oracle."""
 
