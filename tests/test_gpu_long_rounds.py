@@ -1,4 +1,4 @@
-"""GPU: the streaming long-segment round kernel (k_round_long,
+"""GPU: the streaming long-segment round kernel (k_stream,
 csrc/sh_stream.cuh) on every peeled round, including its point-by-point
 path for chunks that overlap three or more segments: the thresholds are
 lowered through SH_LONG_MIN_LIVE / SH_LONG_SEG_MIN so that rounds 2-6 of
